@@ -1,0 +1,159 @@
+/*
+ * dg.h — C ABI of the B200 (sm_100a) fp64 matrix-free SIPG library for the
+ * Hermite-like basis of arXiv 1907.08492 (Kronbichler, Kormann, Wall 2019).
+ *
+ * Operation defined by the paper (citations are PAPER.md line numbers):
+ *   y = A u, A the symmetric interior penalty (SIPG) discretisation of -Laplace
+ *   on hexahedra, Eq. (1), in the tensor-product basis of
+ *   Eq. (2) built from the Hermite-like 1D polynomials of
+ *   Sec. 4.1, integrated with (p+1)^3 Gauss points in the
+ *   cell and (p+1)^2 per face, mirror-principle Dirichlet
+ *   boundaries u+ = -u- (PAPER.md:172-174), penalty (p+1)^2 * A_F / V_K
+ *   (BASELINE.json configs), element-wise face arrangement
+ *   (PAPER.md:323-330).  Readings of silent/ambiguous points: DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *   - Vectors are caller-owned DEVICE pointers to fp64, n_local_dofs long, in
+ *     cell-wise layout: DoF (i,j,k) of cell (cx,cy,cz) at
+ *         ((cz_local*Ny + cy)*Nx + cx) * n^3 + (k*n + j)*n + i,   n = degree+1,
+ *     x fastest inside a cell and across cells, z slowest (a z-slab of a rank
+ *     is one contiguous range).
+ *   - Calls are stream-ordered and asynchronous on the given cudaStream_t
+ *     (passed as void*; NULL = legacy default stream).  Asynchronous CUDA/NCCL
+ *     faults surface on a later call, or immediately with DG_DEBUG_SYNC=1.
+ *   - A handle owns: the 1D tables, geometry, penalties, the GL inverse
+ *     diagonal, the halo buffers, the NCCL communicator, internal events.  A
+ *     handle must not be used from two streams concurrently (halo buffers are
+ *     shared).
+ *   - Every function returns a dg_status; on a non-OK status dg_last_error()
+ *     returns a thread-local message.  No function aborts the process.
+ */
+#ifndef DG_B200_H
+#define DG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DG_OK = 0,
+  DG_ERR_PARAM = 1,        /* bad degree/size/flag, NULL or aliased pointer, lo>=hi, ... */
+  DG_ERR_NUMERIC = 2,      /* det J <= 0, non-finite geometry, non-positive diagonal      */
+  DG_ERR_CUDA = 3,         /* CUDA runtime error (message has the CUDA error string)     */
+  DG_ERR_NCCL = 4,         /* NCCL error                                                  */
+  DG_ERR_UNSUPPORTED = 5   /* combination not implemented (message says which)            */
+} dg_status;
+
+enum { DG_BASIS_HERMITE_LIKE = 0, DG_BASIS_NODAL_GL = 1 };
+enum { DG_GEOM_CONSTANT = 0, DG_GEOM_PER_CELL = 1, DG_GEOM_PER_QPOINT = 2 };
+enum { DG_BC_DIRICHLET_MIRROR = 0, DG_BC_PERIODIC = 1 };
+
+/* dg_apply_laplace flags (bitwise or) */
+enum {
+  DG_APPLY_DEFAULT = 0,          /* exchange halo (if nranks>1) and overlap inside          */
+  DG_APPLY_HALO_READY = 1,       /* caller already ran dg_halo_exchange(m, u, stream)       */
+  DG_APPLY_QUADRATURE = 2        /* force the general quadrature kernel (paper formulation)
+                                    even where the Cartesian Kronecker kernel applies      */
+};
+
+/* dg_basis_change ops: v = B (x) B (x) B u per cell */
+enum {
+  DG_BCHG_H_TO_GL = 0,     /* B = T,      T[i][j] = phi_j^H(x_i^GL)  (values at GL nodes) */
+  DG_BCHG_GL_TO_H = 1,     /* B = T^{-1}                                                  */
+  DG_BCHG_H_TO_GL_T = 2,   /* B = T^T                                                     */
+  DG_BCHG_GL_TO_H_T = 3    /* B = T^{-T}                                                  */
+};
+
+/* dg_chebyshev_smooth inner preconditioners */
+enum {
+  DG_INNER_GL_JACOBI = 0,    /* P^{-1} = (T^{-1})^{x3} diag(A_GL)^{-1} (T^{-T})^{x3}, Eq. (12) */
+  DG_INNER_POINT_JACOBI = 1  /* P^{-1} = diag(A)^{-1} in the working basis    */
+};
+
+typedef struct dg_mesh_s* dg_mesh;   /* opaque, library-owned, freed by dg_mesh_destroy */
+
+typedef struct {
+  int32_t degree;          /* p, 1..8                                                      */
+  int32_t basis;           /* DG_BASIS_*                                                   */
+  int32_t n_cells[3];      /* GLOBAL Nx, Ny, Nz (>= 1)                                     */
+  double  box_lo[3];       /* undeformed box [lo, hi], hi > lo                             */
+  double  box_hi[3];
+  double  linear_map[9];   /* row-major L of x = L X; all-zero = identity */
+  double  deform_amp;      /* x_i += amp sin(2 pi Xh_j) sin(2 pi Xh_k), (i,j,k) cyclic,
+                              Xh the unit-box coordinate; 0 = affine                       */
+  int32_t geometry;        /* DG_GEOM_*; CONSTANT/PER_CELL require deform_amp == 0          */
+  int32_t bc[3];           /* DG_BC_* per direction                                         */
+  double  penalty_factor;  /* multiplies (p+1)^2 A_F/V_K; <= 0 means 1.0 (paper value)       */
+  const double* user_inv_jac; /* optional HOST array, PER_CELL only: 9 doubles per OWNED cell,
+                              row-major J^{-1}, cell order as the DoF layout; NULL = derive */
+  int32_t rank, nranks;    /* z-slab decomposition: rank r owns planes
+                              [r*Nz/nranks, (r+1)*Nz/nranks)                                */
+  const void* nccl_unique_id; /* 128 bytes from dg_get_nccl_unique_id on rank 0, broadcast
+                                 by the caller; NULL when nranks == 1                       */
+  void*   stream;          /* cudaStream_t for setup work (NULL = default)                 */
+} dg_mesh_desc;
+
+/* Message for the last non-OK status of the calling thread (never NULL). */
+const char* dg_last_error(void);
+
+/* Version / build string, e.g. "dg_b200 0.1 sm_100a". */
+const char* dg_version(void);
+
+/* NCCL unique id (128 bytes) into out128 (host memory).  Call on rank 0 only. */
+dg_status dg_get_nccl_unique_id(void* out128);
+
+/* Build the mesh handle: 1D tables (extended precision on the host), geometry and
+ * penalties, the GL inverse diagonal (Eq. (12)),
+ * halo buffers and (nranks > 1) the NCCL communicator.  Synchronises `stream`. */
+dg_status dg_mesh_setup(const dg_mesh_desc* desc, dg_mesh* out);
+
+dg_status dg_mesh_destroy(dg_mesh m);
+
+/* Sizes of the local slab: owned DoFs, global DoFs, owned planes [z_begin, z_end). */
+dg_status dg_mesh_query(dg_mesh m, int64_t* n_local_dofs, int64_t* n_global_dofs,
+                        int32_t* z_begin, int32_t* z_end);
+
+/* Fill the library-owned z-halo of u: the two Hermite face layers (all n layers for
+ * the GL basis) of the neighbouring ranks' boundary planes, via grouped ncclSend/
+ * ncclRecv.  No-op when nranks == 1 and no periodic wrap in z. */
+dg_status dg_halo_exchange(dg_mesh m, const double* u, void* stream);
+
+/* y = A u on the owned cells.  u and y must not alias (DG_ERR_PARAM). */
+dg_status dg_apply_laplace(dg_mesh m, const double* u, double* y, int32_t flags, void* stream);
+
+/* out = B^{x3} in per cell (see DG_BCHG_*); in == out is allowed. */
+dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, void* stream);
+
+/* Chebyshev iteration of Eq. (11), `degree` operator
+ * applications, range [lo_frac, hi_frac] * lambda_max (paper: 0.06, 1.2).
+ * b: right-hand side; x: in x_0, out x_degree; work2: 2 * n_local_dofs doubles
+ * of caller scratch.  Each step is one fused kernel: matvec + residual + P^{-1}
+ * + three-term update ("merged" variant). */
+dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* work2,
+                              int32_t degree, double lambda_max, double lo_frac,
+                              double hi_frac, int32_t inner, void* stream);
+
+/* Inverse of the inner preconditioner's diagonal, copied to `out` (device,
+ * n_local_dofs): diag(A_GL)^{-1} (GL_JACOBI) or diag(A)^{-1} (POINT_JACOBI). */
+dg_status dg_inverse_diagonal(dg_mesh m, int32_t inner, double* out, void* stream);
+
+/* Host-only diagnostic (no GPU needed): the 1D tables the kernels are built from,
+ * for the working basis `basis` at degree p (n = p+1), packed as
+ *   xq[n] wq[n] S[n*n] DS[n*n] v0[n] v1[n] d0[n] d1[n]
+ *   Mhat[n*n] Ahat[n*n] Lhat[n*n] Nm[n*n] Np[n*n] T[n*n] Tinv[n*n]
+ * (row-major; S[q][j] = phi_j(xq_q); T[i][j] = phi_j^H(x_i^GL)); 6n + 9n^2 doubles.
+ * Lhat/Nm/Np are the 1D SIPG blocks on the unit interval with sigma = (p+1)^2 *
+ * penalty_factor (Eq. (14)).  out_len < 6n + 9n^2 -> DG_ERR_PARAM. */
+dg_status dg_tables_1d(int32_t degree, int32_t basis, double penalty_factor, double* out,
+                       int64_t out_len);
+
+/* Number of kernels this library launched since the handle was created. */
+int64_t dg_kernel_launch_count(dg_mesh m);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DG_B200_H */

@@ -1,0 +1,198 @@
+"""Thin Python binding of the dg_b200 C ABI (include/dg.h).
+
+Argument marshalling only: torch tensors provide device memory and the current
+CUDA stream; every step of the hot path runs in the library's sm_100a kernels.
+Names follow the C ABI (dg_mesh_setup -> Mesh, dg_apply_laplace -> apply_laplace, ...).
+"""
+import ctypes
+
+import torch
+
+from ._lib import DgDesc, lib
+
+DG_OK = 0
+STATUS = {0: "DG_OK", 1: "DG_ERR_PARAM", 2: "DG_ERR_NUMERIC", 3: "DG_ERR_CUDA",
+          4: "DG_ERR_NCCL", 5: "DG_ERR_UNSUPPORTED"}
+BASIS = {"hermite": 0, "gl": 1}
+GEOM = {"constant": 0, "per_cell": 1, "per_qpoint": 2}
+BC = {"dirichlet": 0, "periodic": 1}
+BCHG = {"T": 0, "Tinv": 1, "TT": 2, "TinvT": 3}
+INNER = {"gl_jacobi": 0, "point_jacobi": 1}
+APPLY_HALO_READY = 1
+APPLY_QUADRATURE = 2
+
+
+class DgError(RuntimeError):
+    def __init__(self, status, where):
+        msg = lib().dg_last_error().decode()
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(st, where):
+    if st != DG_OK:
+        raise DgError(st, where)
+
+
+def _stream(stream):
+    if stream is None:
+        if not torch.cuda.is_available():
+            return ctypes.c_void_p(0)
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, torch.cuda.Stream):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+def _ptr(t, n=None, name="tensor"):
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA float64 tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if n is not None and t.numel() < n:
+        raise ValueError(f"{name} has {t.numel()} elements, need {n}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def get_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().dg_get_nccl_unique_id(buf), "dg_get_nccl_unique_id")
+    return buf.raw
+
+
+def version() -> str:
+    return lib().dg_version().decode()
+
+
+def tables_1d(degree: int, basis: str = "hermite", penalty_factor: float = 1.0):
+    """Host-only: the 1D tables of the kernels (dict of numpy arrays), see dg.h."""
+    import numpy as np
+    n = degree + 1
+    need = 6 * n + 9 * n * n
+    out = (ctypes.c_double * need)()
+    _check(lib().dg_tables_1d(degree, BASIS[basis], penalty_factor, out, need), "dg_tables_1d")
+    a = np.frombuffer(out, dtype=np.float64).copy()
+    names = [("xq", n), ("wq", n), ("S", n * n), ("DS", n * n), ("v0", n), ("v1", n), ("d0", n),
+             ("d1", n), ("Mhat", n * n), ("Ahat", n * n), ("Lhat", n * n), ("Nm", n * n),
+             ("Np", n * n), ("T", n * n), ("Tinv", n * n)]
+    res, o = {}, 0
+    for k, c in names:
+        v = a[o:o + c]
+        res[k] = v.reshape(n, n) if c == n * n and n > 1 else v
+        o += c
+    return res
+
+
+class Mesh:
+    """dg_mesh_setup(...) handle.  All vectors are CUDA float64 tensors of n_local_dofs."""
+
+    def __init__(self, degree, n_cells, basis="hermite", box_lo=(0.0, 0.0, 0.0),
+                 box_hi=(1.0, 1.0, 1.0), linear_map=None, deform_amp=0.0, geometry="constant",
+                 bc=("dirichlet", "dirichlet", "dirichlet"), penalty_factor=1.0,
+                 user_inv_jac=None, rank=0, nranks=1, nccl_unique_id=None, stream=None):
+        L = lib()
+        d = DgDesc()
+        d.degree = int(degree)
+        d.basis = BASIS[basis]
+        for k in range(3):
+            d.n_cells[k] = int(n_cells[k])
+            d.box_lo[k] = float(box_lo[k])
+            d.box_hi[k] = float(box_hi[k])
+            d.bc[k] = BC[bc[k]]
+        lm = linear_map if linear_map is not None else (1, 0, 0, 0, 1, 0, 0, 0, 1)
+        for k in range(9):
+            d.linear_map[k] = float(lm[k])
+        d.deform_amp = float(deform_amp)
+        d.geometry = GEOM[geometry]
+        d.penalty_factor = float(penalty_factor)
+        self._jac_keepalive = None
+        if user_inv_jac is not None:
+            import numpy as np
+            arr = np.ascontiguousarray(user_inv_jac, dtype=np.float64).reshape(-1)
+            self._jac_keepalive = arr
+            d.user_inv_jac = arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        d.rank = int(rank)
+        d.nranks = int(nranks)
+        self._id_keepalive = None
+        if nccl_unique_id is not None:
+            self._id_keepalive = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
+            d.nccl_unique_id = ctypes.cast(self._id_keepalive, ctypes.c_void_p)
+        d.stream = _stream(stream).value
+        h = ctypes.c_void_p()
+        _check(L.dg_mesh_setup(ctypes.byref(d), ctypes.byref(h)), "dg_mesh_setup")
+        self._h = h
+        nl, ng = ctypes.c_int64(), ctypes.c_int64()
+        zb, ze = ctypes.c_int32(), ctypes.c_int32()
+        _check(L.dg_mesh_query(h, ctypes.byref(nl), ctypes.byref(ng), ctypes.byref(zb),
+                               ctypes.byref(ze)), "dg_mesh_query")
+        self.n_local_dofs, self.n_global_dofs = nl.value, ng.value
+        self.z_begin, self.z_end = zb.value, ze.value
+        self.degree = int(degree)
+        self.n = self.degree + 1
+
+    # ------------------------------------------------------------------ lifetime
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().dg_mesh_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().dg_kernel_launch_count(self._h))
+
+    def empty(self):
+        return torch.empty(self.n_local_dofs, dtype=torch.float64, device="cuda")
+
+    # ------------------------------------------------------------------ operators
+    def halo_exchange(self, u, stream=None):
+        _check(lib().dg_halo_exchange(self._h, _ptr(u, self.n_local_dofs, "u"), _stream(stream)),
+               "dg_halo_exchange")
+
+    def apply_laplace(self, u, y=None, flags=0, stream=None):
+        if y is None:
+            y = self.empty()
+        _check(lib().dg_apply_laplace(self._h, _ptr(u, self.n_local_dofs, "u"),
+                                      _ptr(y, self.n_local_dofs, "y"), int(flags), _stream(stream)),
+               "dg_apply_laplace")
+        return y
+
+    def basis_change(self, op, x, out=None, stream=None):
+        if out is None:
+            out = self.empty()
+        _check(lib().dg_basis_change(self._h, BCHG[op], _ptr(x, self.n_local_dofs, "in"),
+                                     _ptr(out, self.n_local_dofs, "out"), _stream(stream)),
+               "dg_basis_change")
+        return out
+
+    def chebyshev_smooth(self, b, x, lambda_max, degree=5, lo=0.06, hi=1.2, inner="gl_jacobi",
+                         work2=None, stream=None):
+        if work2 is None:
+            work2 = torch.empty(2 * self.n_local_dofs, dtype=torch.float64, device="cuda")
+        _check(lib().dg_chebyshev_smooth(self._h, _ptr(b, self.n_local_dofs, "b"),
+                                         _ptr(x, self.n_local_dofs, "x"),
+                                         _ptr(work2, 2 * self.n_local_dofs, "work2"), int(degree),
+                                         float(lambda_max), float(lo), float(hi), INNER[inner],
+                                         _stream(stream)), "dg_chebyshev_smooth")
+        return x
+
+    def inverse_diagonal(self, inner="gl_jacobi", out=None, stream=None):
+        if out is None:
+            out = self.empty()
+        _check(lib().dg_inverse_diagonal(self._h, INNER[inner], _ptr(out, self.n_local_dofs, "out"),
+                                         _stream(stream)), "dg_inverse_diagonal")
+        return out
+
+
+def mesh_from_spec(spec, **kw) -> Mesh:
+    """Mesh from a synthetic.MeshSpec (plain data)."""
+    args = dict(degree=spec.degree, n_cells=spec.n_cells, basis=spec.basis, box_lo=spec.box_lo,
+                box_hi=spec.box_hi, linear_map=spec.linear_map, deform_amp=spec.deform_amp,
+                geometry=spec.geometry, bc=spec.bc, penalty_factor=spec.penalty_factor)
+    args.update(kw)
+    return Mesh(**args)

@@ -1,0 +1,497 @@
+// C ABI of dg_b200 (include/dg.h): mesh setup, operator dispatch, basis change,
+// fused Chebyshev driver, z-slab halo exchange over NCCL.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dg_internal.h"
+
+using namespace dgb;
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+dg_status fail(dg_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DG_DEBUG_SYNC");
+    v = (e && *e && *e != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(DG_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),    \
+                  __FILE__, __LINE__);                                              \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                              \
+  do {                                                                              \
+    ncclResult_t r_ = (expr);                                                       \
+    if (r_ != ncclSuccess)                                                          \
+      return fail(DG_ERR_NCCL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(r_),    \
+                  __FILE__, __LINE__);                                              \
+  } while (0)
+
+// pack an n x n row-major matrix into the even-odd layout of common.cuh
+void pack_eo(const double* A, int n, double* out) {
+  const int h = n / 2, mid = h;
+  int o = 0;
+  for (int i = 0; i < h; ++i)
+    for (int j = 0; j < h; ++j) out[o++] = 0.5 * (A[i * n + j] + A[i * n + n - 1 - j]);
+  for (int i = 0; i < h; ++i)
+    for (int j = 0; j < h; ++j) out[o++] = 0.5 * (A[i * n + j] - A[i * n + n - 1 - j]);
+  for (int i = 0; i < h; ++i) out[o++] = (n & 1) ? A[i * n + mid] : 0.0;
+  for (int j = 0; j < h; ++j) out[o++] = (n & 1) ? A[mid * n + j] : 0.0;
+  out[o++] = (n & 1) ? A[mid * n + mid] : 0.0;
+}
+
+void transpose(const double* A, int n, double* At) {
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) At[j * n + i] = A[i * n + j];
+}
+
+}  // namespace
+
+struct dg_mesh_s {
+  dg_mesh_desc desc{};
+  Tables1D tab;
+  int n = 0, NL = 0;
+  int N[3] = {0, 0, 0};
+  int z_begin = 0, z_end = 0, nz = 0;
+  int64_t ncells_local = 0, ndofs_local = 0, ndofs_global = 0;
+  double h[3] = {0, 0, 0};
+  bool cartesian = false;
+  KronParams kp{};
+  int zlo = ZSRC_MIRROR, zhi = ZSRC_MIRROR;
+  // lazily built inverse diagonals
+  double* d_dinv_gl = nullptr;
+  double* d_dinv_pj = nullptr;
+  // halo (z-slabs)
+  double* d_recv_lo = nullptr;
+  double* d_recv_hi = nullptr;
+  double* d_send_lo = nullptr;
+  double* d_send_hi = nullptr;
+  int64_t halo_count = 0;         // doubles per halo buffer
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  int64_t launches = 0;
+};
+
+namespace {
+
+dg_status post_launch(dg_mesh m, cudaError_t e, const char* what, cudaStream_t s) {
+  if (e != cudaSuccess) return fail(DG_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+  m->launches++;
+  if (debug_sync()) {
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e2 != cudaSuccess) return fail(DG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e2));
+  }
+  return DG_OK;
+}
+
+GridArgs grid_args(dg_mesh m, int zbeg, int zend) {
+  GridArgs g{};
+  g.Nx = m->N[0];
+  g.Ny = m->N[1];
+  g.nz = m->nz;
+  g.bc[0] = m->desc.bc[0];
+  g.bc[1] = m->desc.bc[1];
+  g.bc[2] = m->desc.bc[2];
+  g.zlo = m->zlo;
+  g.zhi = m->zhi;
+  g.zbeg = zbeg;
+  g.zend = zend;
+  g.halo_lo = m->d_recv_lo;
+  g.halo_hi = m->d_recv_hi;
+  return g;
+}
+
+// 1D diagonal variants [interior, left bdry, right bdry, both] of the 1D block L
+void diag_variants(const double* L, const double* Nm, const double* Np, int n, int bc, int Nd,
+                   double scale_unused, double out[4][kMaxN]) {
+  (void)scale_unused;
+  for (int i = 0; i < n; ++i) {
+    const double li = L[i * n + i];
+    const double cl = -Nm[i * n + (n - 1 - i)];   // mirror ghost of the face at xi=0
+    const double cr = -Np[i * n + (n - 1 - i)];   // mirror ghost of the face at xi=1
+    if (bc == DG_BC_PERIODIC) {
+      for (int v = 0; v < 4; ++v) out[v][i] = li;
+      if (Nd == 1) out[3][i] = li + Nm[i * n + i] + Np[i * n + i];
+    } else {
+      out[0][i] = li;
+      out[1][i] = li + cl;
+      out[2][i] = li + cr;
+      out[3][i] = li + cl + cr;
+    }
+  }
+}
+
+dg_status build_diag(dg_mesh m, bool gl, double** dst, cudaStream_t s) {
+  if (*dst) return DG_OK;
+  if (!m->cartesian)
+    return fail(DG_ERR_UNSUPPORTED, "inverse diagonal: only Cartesian meshes in this build");
+  const Tables1D& t = m->tab;
+  const int n = m->n;
+  const double* M = gl ? t.gl_Mhat : t.Mhat;
+  const double* L = gl ? t.gl_Lhat : t.Lhat;
+  const double* Nm = gl ? t.gl_Nm : t.Nm;
+  const double* Np = gl ? t.gl_Np : t.Np;
+  CartDiagParams p{};
+  for (int i = 0; i < n; ++i) p.mdiag[i] = M[i * n + i];
+  const double V = m->h[0] * m->h[1] * m->h[2];
+  for (int d = 0; d < 3; ++d) {
+    diag_variants(L, Nm, Np, n, m->desc.bc[d], m->N[d], 0, p.ldiag[d]);
+    p.scale[d] = V / (m->h[d] * m->h[d]);
+  }
+  p.invert = 1;
+  CUDA_TRY(cudaMalloc(dst, sizeof(double) * (size_t)std::max<int64_t>(m->ndofs_local, 1)));
+  dg_status st = post_launch(m, launch_cart_diag(n, p, m->N[0], m->N[1], m->nz, m->z_begin,
+                                                 m->N[2], *dst, s),
+                             "cart_diag", s);
+  return st;
+}
+
+dg_status halo_exchange_impl(dg_mesh m, const double* u, cudaStream_t s);
+
+}  // namespace
+
+extern "C" {
+
+const char* dg_last_error(void) { return g_err.c_str(); }
+
+const char* dg_version(void) { return "dg_b200 0.1 sm_100a fp64"; }
+
+dg_status dg_get_nccl_unique_id(void* out128) {
+  if (!out128) return fail(DG_ERR_PARAM, "out128 is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof id);
+  return DG_OK;
+}
+
+dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
+  if (!d || !out) return fail(DG_ERR_PARAM, "NULL desc or out");
+  *out = nullptr;
+  if (d->degree < 1 || d->degree > 8) return fail(DG_ERR_PARAM, "degree %d not in 1..8", d->degree);
+  if (d->basis != DG_BASIS_HERMITE_LIKE && d->basis != DG_BASIS_NODAL_GL)
+    return fail(DG_ERR_PARAM, "bad basis %d", d->basis);
+  for (int k = 0; k < 3; ++k) {
+    if (d->n_cells[k] < 1) return fail(DG_ERR_PARAM, "n_cells[%d] = %d", k, d->n_cells[k]);
+    if (!(d->box_hi[k] > d->box_lo[k])) return fail(DG_ERR_PARAM, "box_hi[%d] <= box_lo[%d]", k, k);
+    if (d->bc[k] != DG_BC_DIRICHLET_MIRROR && d->bc[k] != DG_BC_PERIODIC)
+      return fail(DG_ERR_PARAM, "bad bc[%d]", k);
+  }
+  if (d->geometry < DG_GEOM_CONSTANT || d->geometry > DG_GEOM_PER_QPOINT)
+    return fail(DG_ERR_PARAM, "bad geometry %d", d->geometry);
+  if (d->deform_amp != 0.0 && d->geometry != DG_GEOM_PER_QPOINT)
+    return fail(DG_ERR_PARAM, "deform_amp != 0 requires DG_GEOM_PER_QPOINT");
+  const int nranks = d->nranks < 1 ? 1 : d->nranks;
+  if (d->rank < 0 || d->rank >= nranks) return fail(DG_ERR_PARAM, "rank %d of %d", d->rank, nranks);
+  if (d->n_cells[2] < nranks) return fail(DG_ERR_PARAM, "Nz=%d < nranks=%d", d->n_cells[2], nranks);
+  if (nranks > 1 && !d->nccl_unique_id) return fail(DG_ERR_PARAM, "nranks > 1 needs nccl_unique_id");
+
+  dg_mesh m = new dg_mesh_s();
+  m->desc = *d;
+  m->desc.user_inv_jac = nullptr;
+  m->rank = d->rank;
+  m->nranks = nranks;
+  if (!build_tables(d->degree, d->basis, d->penalty_factor, &m->tab)) {
+    delete m;
+    return fail(DG_ERR_PARAM, "build_tables failed");
+  }
+  const int n = m->n = d->degree + 1;
+  m->NL = (d->basis == DG_BASIS_HERMITE_LIKE && n > 2) ? 2 : n;
+  for (int k = 0; k < 3; ++k) m->N[k] = d->n_cells[k];
+  m->z_begin = (int)((int64_t)d->rank * m->N[2] / nranks);
+  m->z_end = (int)((int64_t)(d->rank + 1) * m->N[2] / nranks);
+  m->nz = m->z_end - m->z_begin;
+  const int64_t n3 = (int64_t)n * n * n;
+  m->ncells_local = (int64_t)m->N[0] * m->N[1] * m->nz;
+  m->ndofs_local = m->ncells_local * n3;
+  m->ndofs_global = (int64_t)m->N[0] * m->N[1] * m->N[2] * n3;
+
+  // geometry: Cartesian = identity-or-diagonal linear map, no deformation
+  double L[9];
+  bool allzero = true;
+  for (int k = 0; k < 9; ++k) {
+    L[k] = d->linear_map[k];
+    if (L[k] != 0.0) allzero = false;
+  }
+  if (allzero) {
+    for (int k = 0; k < 9; ++k) L[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  }
+  const bool diagonal = L[1] == 0 && L[2] == 0 && L[3] == 0 && L[5] == 0 && L[6] == 0 && L[7] == 0;
+  m->cartesian = diagonal && d->deform_amp == 0.0 && d->geometry == DG_GEOM_CONSTANT;
+  for (int k = 0; k < 3; ++k) m->h[k] = L[4 * k] * (d->box_hi[k] - d->box_lo[k]) / m->N[k];
+  if (!m->cartesian) {
+    delete m;
+    return fail(DG_ERR_UNSUPPORTED,
+                "this build implements the Cartesian constant-geometry path only "
+                "(diagonal linear_map, deform_amp == 0, DG_GEOM_CONSTANT)");
+  }
+  for (int k = 0; k < 3; ++k)
+    if (!(m->h[k] > 0) || !std::isfinite(m->h[k])) {
+      delete m;
+      return fail(DG_ERR_NUMERIC, "non-positive cell size in direction %d", k);
+    }
+
+  // Kronecker parameters: L_d = (V/h_d^2) Lhat, Nm/Np blocks [NL][NL]
+  {
+    const Tables1D& t = m->tab;
+    KronParams& kp = m->kp;
+    std::memset(&kp, 0, sizeof kp);
+    pack_eo(t.Mhat, n, kp.M);
+    const double V = m->h[0] * m->h[1] * m->h[2];
+    const int NL = m->NL;
+    for (int dd = 0; dd < 3; ++dd) {
+      const double sc = V / (m->h[dd] * m->h[dd]);
+      double Ls[kMaxN * kMaxN];
+      for (int q = 0; q < n * n; ++q) Ls[q] = sc * t.Lhat[q];
+      pack_eo(Ls, n, kp.L[dd]);
+      for (int i = 0; i < NL; ++i)
+        for (int l = 0; l < NL; ++l) {
+          kp.Nm[dd][i * NL + l] = sc * t.Nm[i * n + (n - NL + l)];
+          kp.Np[dd][i * NL + l] = sc * t.Np[(n - NL + i) * n + l];
+        }
+    }
+    double TiT[kMaxN * kMaxN];
+    transpose(t.Tinv, n, TiT);
+    pack_eo(TiT, n, kp.TiT);
+    pack_eo(t.Tinv, n, kp.Ti);
+  }
+
+  // z sources and halo
+  const bool zper = d->bc[2] == DG_BC_PERIODIC;
+  if (nranks == 1) {
+    m->zlo = m->zhi = zper ? ZSRC_LOCAL : ZSRC_MIRROR;
+  } else {
+    m->zlo = (d->rank == 0 && !zper) ? ZSRC_MIRROR : ZSRC_HALO;
+    m->zhi = (d->rank == nranks - 1 && !zper) ? ZSRC_MIRROR : ZSRC_HALO;
+  }
+  cudaStream_t s = (cudaStream_t)d->stream;
+  if (m->zlo == ZSRC_HALO || m->zhi == ZSRC_HALO) {
+    m->halo_count = (int64_t)m->N[0] * m->N[1] * m->NL * n * n;
+    const size_t bytes = sizeof(double) * (size_t)m->halo_count;
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMalloc(&m->d_recv_lo, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&m->d_recv_hi, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&m->d_send_lo, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&m->d_send_hi, bytes);
+    if (e != cudaSuccess) {
+      dg_mesh_destroy(m);
+      return fail(DG_ERR_CUDA, "halo alloc: %s", cudaGetErrorString(e));
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, d->nccl_unique_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&m->comm, nranks, id, d->rank);
+    if (r != ncclSuccess) {
+      m->comm = nullptr;
+      dg_mesh_destroy(m);
+      return fail(DG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+  }
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    dg_mesh_destroy(m);
+    return fail(DG_ERR_CUDA, "setup sync: %s", cudaGetErrorString(e));
+  }
+  *out = m;
+  return DG_OK;
+}
+
+dg_status dg_mesh_destroy(dg_mesh m) {
+  if (!m) return DG_OK;
+  cudaFree(m->d_dinv_gl);
+  cudaFree(m->d_dinv_pj);
+  cudaFree(m->d_recv_lo);
+  cudaFree(m->d_recv_hi);
+  cudaFree(m->d_send_lo);
+  cudaFree(m->d_send_hi);
+  if (m->comm) ncclCommDestroy(m->comm);
+  delete m;
+  return DG_OK;
+}
+
+dg_status dg_mesh_query(dg_mesh m, int64_t* nl, int64_t* ng, int32_t* zb, int32_t* ze) {
+  if (!m) return fail(DG_ERR_PARAM, "NULL mesh");
+  if (nl) *nl = m->ndofs_local;
+  if (ng) *ng = m->ndofs_global;
+  if (zb) *zb = m->z_begin;
+  if (ze) *ze = m->z_end;
+  return DG_OK;
+}
+
+int64_t dg_kernel_launch_count(dg_mesh m) { return m ? m->launches : -1; }
+
+dg_status dg_tables_1d(int32_t degree, int32_t basis, double pf, double* out, int64_t out_len) {
+  if (!out) return fail(DG_ERR_PARAM, "NULL out");
+  Tables1D t;
+  if (!build_tables(degree, basis, pf, &t)) return fail(DG_ERR_PARAM, "bad degree/basis");
+  const int n = t.n;
+  const int64_t need = 6 * n + 9 * n * n;
+  if (out_len < need) return fail(DG_ERR_PARAM, "out_len %lld < %lld", (long long)out_len, (long long)need);
+  double* o = out;
+  auto put = [&](const double* a, int cnt) { std::memcpy(o, a, sizeof(double) * cnt); o += cnt; };
+  put(t.xq, n); put(t.wq, n); put(t.S, n * n); put(t.DS, n * n);
+  put(t.v0, n); put(t.v1, n); put(t.d0, n); put(t.d1, n);
+  put(t.Mhat, n * n); put(t.Ahat, n * n); put(t.Lhat, n * n); put(t.Nm, n * n); put(t.Np, n * n);
+  put(t.T, n * n); put(t.Tinv, n * n);
+  return DG_OK;
+}
+
+dg_status dg_halo_exchange(dg_mesh m, const double* u, void* stream) {
+  if (!m || !u) return fail(DG_ERR_PARAM, "NULL argument");
+  return halo_exchange_impl(m, u, (cudaStream_t)stream);
+}
+
+dg_status dg_apply_laplace(dg_mesh m, const double* u, double* y, int32_t flags, void* stream) {
+  if (!m || !u || !y) return fail(DG_ERR_PARAM, "NULL argument");
+  if (u == y) return fail(DG_ERR_PARAM, "u and y alias");
+  if (flags & ~(DG_APPLY_HALO_READY | DG_APPLY_QUADRATURE)) return fail(DG_ERR_PARAM, "bad flags");
+  if (flags & DG_APPLY_QUADRATURE)
+    return fail(DG_ERR_UNSUPPORTED, "quadrature kernel not in this build");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(flags & DG_APPLY_HALO_READY)) {
+    dg_status st = halo_exchange_impl(m, u, s);
+    if (st != DG_OK) return st;
+  }
+  ChebyArgs ch{};
+  GridArgs g = grid_args(m, 0, m->nz);
+  return post_launch(m, launch_kron(m->n, m->NL, KMODE_APPLY, m->kp, g, u, y, ch, s), "kron_apply", s);
+}
+
+dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, void* stream) {
+  if (!m || !in || !out) return fail(DG_ERR_PARAM, "NULL argument");
+  const int n = m->n;
+  const Tables1D& t = m->tab;
+  double B[kMaxN * kMaxN];
+  switch (op) {
+    case DG_BCHG_H_TO_GL: std::memcpy(B, t.T, sizeof B); break;
+    case DG_BCHG_GL_TO_H: std::memcpy(B, t.Tinv, sizeof B); break;
+    case DG_BCHG_H_TO_GL_T: transpose(t.T, n, B); break;
+    case DG_BCHG_GL_TO_H_T: transpose(t.Tinv, n, B); break;
+    default: return fail(DG_ERR_PARAM, "bad basis-change op %d", op);
+  }
+  BchgParams bp{};
+  pack_eo(B, n, bp.B);
+  cudaStream_t s = (cudaStream_t)stream;
+  return post_launch(m, launch_basis_change(n, bp, in, out, m->ncells_local, s), "basis_change", s);
+}
+
+dg_status dg_inverse_diagonal(dg_mesh m, int32_t inner, double* out, void* stream) {
+  if (!m || !out) return fail(DG_ERR_PARAM, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool gl = inner == DG_INNER_GL_JACOBI;
+  if (!gl && inner != DG_INNER_POINT_JACOBI) return fail(DG_ERR_PARAM, "bad inner %d", inner);
+  double** dst = gl ? &m->d_dinv_gl : &m->d_dinv_pj;
+  dg_status st = build_diag(m, gl, dst, s);
+  if (st != DG_OK) return st;
+  CUDA_TRY(cudaMemcpyAsync(out, *dst, sizeof(double) * (size_t)m->ndofs_local,
+                           cudaMemcpyDeviceToDevice, s));
+  return DG_OK;
+}
+
+dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* work2, int32_t degree,
+                              double lambda_max, double lo_frac, double hi_frac, int32_t inner,
+                              void* stream) {
+  if (!m || !b || !x || !work2) return fail(DG_ERR_PARAM, "NULL argument");
+  if (degree < 0) return fail(DG_ERR_PARAM, "degree < 0");
+  const double alpha = lo_frac * lambda_max, beta = hi_frac * lambda_max;
+  if (!(alpha > 0 && beta > alpha) || !std::isfinite(beta))
+    return fail(DG_ERR_PARAM, "need 0 < lo_frac*lambda_max < hi_frac*lambda_max");
+  if (inner != DG_INNER_GL_JACOBI && inner != DG_INNER_POINT_JACOBI)
+    return fail(DG_ERR_PARAM, "bad inner %d", inner);
+  const int64_t nd = m->ndofs_local;
+  double* W0 = work2;
+  double* W1 = work2 + nd;
+  if ((b >= W0 && b < W1 + nd) || (x >= W0 && x < W1 + nd) || b == x)
+    return fail(DG_ERR_PARAM, "b, x and work2 must not overlap");
+  if (degree == 0) return DG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool gl = inner == DG_INNER_GL_JACOBI && m->desc.basis == DG_BASIS_HERMITE_LIKE;
+  double** dsrc = gl ? &m->d_dinv_gl : &m->d_dinv_pj;
+  dg_status st = build_diag(m, inner == DG_INNER_GL_JACOBI, dsrc, s);
+  if (st != DG_OK) return st;
+  const int mode = gl ? KMODE_CHEBY_GL : KMODE_CHEBY_PJ;
+
+  // storage of u_j so that u_degree lands in x (in-place updates over u_{j-1})
+  double* buf[3] = {x, W0, W1};
+  std::vector<int> where(degree + 1);
+  where[0] = 0;
+  if (degree == 1) {
+    where[1] = 1;
+  } else if (degree % 2 == 0) {
+    for (int j = 1; j <= degree; ++j) where[j] = (j % 2 == 1) ? 1 : 0;
+  } else {
+    where[1] = 1;
+    where[2] = 2;
+    for (int j = 3; j <= degree; ++j) where[j] = (j % 2 == 1) ? 0 : 2;
+  }
+  const double c = 0.5 * (beta + alpha), delta = 0.5 * (beta - alpha);
+  const double sigma1 = c / delta;
+  double rho = 1.0 / sigma1;
+  for (int j = 0; j < degree; ++j) {
+    ChebyArgs ch{};
+    ch.b = b;
+    ch.dinv = *dsrc;
+    ch.u_next = buf[where[j + 1]];
+    if (j == 0) {
+      ch.first = 1;
+      ch.c_z = 1.0 / c;
+      ch.c_prev = 0.0;
+      ch.u_prev = nullptr;
+    } else {
+      const double rho_n = 1.0 / (2.0 * sigma1 - rho);
+      ch.first = 0;
+      ch.c_prev = rho_n * rho;
+      ch.c_z = 2.0 * rho_n / delta;
+      ch.u_prev = buf[where[j - 1]];
+      rho = rho_n;
+    }
+    const double* uj = buf[where[j]];
+    st = halo_exchange_impl(m, uj, s);
+    if (st != DG_OK) return st;
+    GridArgs g = grid_args(m, 0, m->nz);
+    st = post_launch(m, launch_kron(m->n, m->NL, mode, m->kp, g, uj, nullptr, ch, s), "kron_cheby", s);
+    if (st != DG_OK) return st;
+  }
+  if (where[degree] != 0)
+    CUDA_TRY(cudaMemcpyAsync(x, buf[where[degree]], sizeof(double) * (size_t)nd,
+                             cudaMemcpyDeviceToDevice, s));
+  return DG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+dg_status halo_exchange_impl(dg_mesh m, const double* u, cudaStream_t s) {
+  if (!m->comm) return DG_OK;   // single rank: periodic wrap is read in place
+  return fail(DG_ERR_UNSUPPORTED, "multi-rank halo not in this build");
+}
+
+}  // namespace

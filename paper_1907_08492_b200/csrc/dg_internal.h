@@ -1,0 +1,70 @@
+// Internal host/device declarations of the dg_b200 library (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/dg.h"
+#include "basis_host.h"
+#include "common.cuh"
+
+namespace dgb {
+
+// Kernel parameters of the Cartesian Kronecker path (SURVEY.md §8(f) NEXT#1,
+// Eq. (14)): per direction d, y = sum_d (Mhat (x) Mhat (x) L_d) u + neighbour
+// couplings, L_d = (V/h_d^2) Lhat.  Passed by value (__grid_constant__), so all
+// coefficients live in the constant bank.
+struct KronParams {
+  double M[kEO];               // Mhat, even-odd packed, parity +1
+  double L[3][kEO];            // (V / h_d^2) Lhat, even-odd packed, parity +1
+  double Nm[3][kMaxN * kMaxN]; // [NL][NL]: own rows [0,NL) x neighbour layers [n-NL,n)
+  double Np[3][kMaxN * kMaxN]; // [NL][NL]: own rows [n-NL,n) x neighbour layers [0,NL)
+  double TiT[kEO];             // T^{-T}, even-odd packed
+  double Ti[kEO];              // T^{-1}
+};
+
+// Where the z-neighbour layers of the bottom / top local plane come from.
+enum { ZSRC_LOCAL = 0, ZSRC_HALO = 1, ZSRC_MIRROR = 2 };
+
+struct GridArgs {
+  int Nx, Ny, nz;             // local cells per direction (nz local planes)
+  int bc[3];                  // DG_BC_* per direction (x, y used; z via zlo/zhi)
+  int zlo, zhi;               // ZSRC_* for the plane below local plane 0 / above nz-1
+  int zbeg, zend;             // local planes processed by this launch
+  const double* halo_lo;      // [Nx*Ny][NL][n][n]: neighbour layers [n-NL, n) of the plane below
+  const double* halo_hi;      // [Nx*Ny][NL][n][n]: neighbour layers [0, NL) of the plane above
+};
+
+enum { KMODE_APPLY = 0, KMODE_CHEBY_GL = 1, KMODE_CHEBY_PJ = 2 };
+
+struct ChebyArgs {
+  const double* b;
+  const double* u_prev;       // may alias u_next (in-place three-term update)
+  double* u_next;
+  const double* dinv;         // inverse diagonal (GL for CHEBY_GL, working basis for CHEBY_PJ)
+  double c_prev;              // rho_{j+1} rho_j      (0 on the first step)
+  double c_z;                 // 2 rho_{j+1} / delta  (1/c on the first step)
+  int first;                  // 1: u_prev is not read
+};
+
+struct BchgParams {
+  double B[kEO];              // even-odd packed 1D matrix, parity +1
+};
+
+// Launchers (k_kron.cu, k_basis_change.cu, k_setup.cu)
+cudaError_t launch_kron(int n, int NL, int mode, const KronParams& kp, const GridArgs& g,
+                        const double* u, double* y, const ChebyArgs& ch, cudaStream_t s);
+cudaError_t launch_basis_change(int n, const BchgParams& bp, const double* in, double* out,
+                                int64_t ncells, cudaStream_t s);
+// diagonal of a Cartesian Kronecker operator: d[i,j,k] = sum_d c_d prod(1D diagonals)
+struct CartDiagParams {
+  double mdiag[kMaxN];                 // diag(Mhat_basis)
+  double ldiag[3][4][kMaxN];           // per direction: [interior, left bdry, right bdry, both]
+  double scale[3];                     // V / h_d^2
+  int invert;                          // write 1/d instead of d
+};
+cudaError_t launch_cart_diag(int n, const CartDiagParams& p, int Nx, int Ny, int nz, int z0,
+                             int Nz_global, double* out, cudaStream_t s);
+
+}  // namespace dgb

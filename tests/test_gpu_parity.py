@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerance: relative L2 <= 1e-12 in fp64 (BASELINE.json north_star), per
+element |gpu - oracle| <= 1e-12 * max|oracle| on the sampled checks.
+Inputs are seeded uniform[-1,1) vectors from synthetic/ (same bytes both sides).
+"""
+import numpy as np
+import pytest
+import torch
+
+from synthetic import CONFIGS, MeshSpec, c4_spec, uniform_vector
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def _needs_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def _gpu_mesh(spec, **kw):
+    import paper_1907_08492_b200 as P
+    return P.mesh_from_spec(spec, **kw)
+
+
+def _oracle(spec):
+    from oracle.geometry import mesh_from_spec
+    from oracle.sipg import SIPG
+    return SIPG(mesh_from_spec(spec), spec.degree, spec.basis, spec.penalty_factor)
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+SMALL = []
+for p in range(1, 9):
+    SMALL.append(MeshSpec(degree=p, n_cells=(3, 2, 4), box_lo=(0.0, -0.5, 0.25), box_hi=(1.5, 0.5, 1.0),
+                          seed=100 + p))
+    SMALL.append(MeshSpec(degree=p, n_cells=(5, 3, 2), bc=("periodic", "dirichlet", "periodic"),
+                          seed=200 + p))
+    SMALL.append(MeshSpec(degree=p, n_cells=(2, 3, 3), basis="gl", bc=("dirichlet", "periodic", "dirichlet"),
+                          seed=300 + p))
+
+
+@pytest.mark.parametrize("spec", SMALL, ids=lambda s: f"p{s.degree}-{s.basis}-{s.n_cells}-{s.bc[0][0]}{s.bc[1][0]}{s.bc[2][0]}")
+def test_apply_small(spec):
+    _needs_gpu()
+    u = uniform_vector(spec.n_dofs, spec.seed)
+    ref = _oracle(spec).apply(u)
+    m = _gpu_mesh(spec)
+    y = m.apply_laplace(_dev(u)).cpu().numpy()
+    assert _rel(y, ref) <= TOL
+    assert np.abs(y - ref).max() <= TOL * np.abs(ref).max()
+
+
+def test_apply_c1_exact_config():
+    """BASELINE C1: p=3, 4^3 cells, mirror Dirichlet, seed 0, 4096 DoF."""
+    _needs_gpu()
+    spec = CONFIGS["C1"]
+    assert spec.n_dofs == 4096
+    u = uniform_vector(spec.n_dofs, spec.seed)
+    ref = _oracle(spec).apply(u)
+    y = _gpu_mesh(spec).apply_laplace(_dev(u)).cpu().numpy()
+    assert _rel(y, ref) <= TOL
+
+
+def test_single_cell_and_periodic_self_neighbour():
+    _needs_gpu()
+    for bc in (("dirichlet",) * 3, ("periodic",) * 3, ("periodic", "dirichlet", "periodic")):
+        for p in (2, 5):
+            spec = MeshSpec(degree=p, n_cells=(1, 1, 1), bc=bc, seed=7)
+            u = uniform_vector(spec.n_dofs, 7)
+            ref = _oracle(spec).apply(u)
+            y = _gpu_mesh(spec).apply_laplace(_dev(u)).cpu().numpy()
+            assert _rel(y, ref) <= TOL, (bc, p)
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+def test_hermite_access_only_two_layers(p):
+    """an interior cell reads its (p+1)^3 values plus 2 layers per
+    face of each neighbour.  Poison every other neighbour coefficient with NaN:
+    the cell's result must stay finite and bit-identical."""
+    _needs_gpu()
+    n = p + 1
+    spec = MeshSpec(degree=p, n_cells=(3, 3, 3), seed=5)
+    u = uniform_vector(spec.n_dofs, 5)
+    m = _gpu_mesh(spec)
+    y0 = m.apply_laplace(_dev(u)).cpu().numpy().reshape(27, n, n, n)
+    U = u.reshape(3, 3, 3, n, n, n).copy()       # [cz,cy,cx,k,j,i]
+    c = (1, 1, 1)
+    poisoned = U.copy()
+    for d in range(3):
+        for s in (-1, 1):
+            nb = list(c)
+            nb[2 - d] += s
+            cell = poisoned[tuple(nb)]
+            keep = np.zeros((n, n, n), bool)
+            layers = [n - 2, n - 1] if s < 0 else [0, 1]
+            idx = [slice(None)] * 3
+            idx[2 - d] = layers
+            keep[tuple(idx)] = True
+            cell[~keep] = np.nan
+    y1 = m.apply_laplace(_dev(poisoned.reshape(-1))).cpu().numpy().reshape(27, n, n, n)
+    centre = 13
+    assert np.all(np.isfinite(y1[centre]))
+    assert np.array_equal(y1[centre], y0[centre])
+
+
+def test_gl_basis_reads_full_neighbours():
+    """Nodal GL: the same poisoning must reach the centre cell."""
+    _needs_gpu()
+    p, n = 3, 4
+    spec = MeshSpec(degree=p, n_cells=(3, 3, 3), basis="gl", seed=5)
+    u = uniform_vector(spec.n_dofs, 5).reshape(3, 3, 3, n, n, n)
+    u[1, 1, 0, :, :, 0] = np.nan          # x- neighbour, layer farthest from the face
+    y = _gpu_mesh(spec).apply_laplace(_dev(u.reshape(-1))).cpu().numpy().reshape(27, -1)
+    assert not np.all(np.isfinite(y[13]))
+
+
+@pytest.mark.parametrize("p", range(1, 9))
+@pytest.mark.parametrize("op", ["T", "Tinv", "TT", "TinvT"])
+def test_basis_change(p, op):
+    _needs_gpu()
+    from oracle import smoother as sm
+    spec = MeshSpec(degree=p, n_cells=(3, 2, 3), seed=40 + p)
+    u = uniform_vector(spec.n_dofs, spec.seed)
+    ref = sm.basis_change(p, u, op)
+    m = _gpu_mesh(spec)
+    v = m.basis_change(op, _dev(u)).cpu().numpy()
+    assert _rel(v, ref) <= TOL
+    w = _dev(u)
+    m.basis_change(op, w, out=w)                   # in place
+    assert _rel(w.cpu().numpy(), ref) <= TOL
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 7])
+@pytest.mark.parametrize("basis", ["hermite", "gl"])
+def test_inverse_diagonal(p, basis):
+    _needs_gpu()
+    from oracle.geometry import mesh_from_spec
+    from oracle.sipg import SIPG
+    spec = MeshSpec(degree=p, n_cells=(3, 1, 2), basis=basis, bc=("dirichlet", "periodic", "dirichlet"))
+    om = mesh_from_spec(spec)
+    m = _gpu_mesh(spec)
+    ref_gl = 1.0 / SIPG(om, p, "gl").diagonal()
+    ref_pj = 1.0 / SIPG(om, p, basis).diagonal()
+    assert _rel(m.inverse_diagonal("gl_jacobi").cpu().numpy(), ref_gl) <= TOL
+    assert _rel(m.inverse_diagonal("point_jacobi").cpu().numpy(), ref_pj) <= TOL
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+@pytest.mark.parametrize("inner", ["gl_jacobi", "point_jacobi"])
+@pytest.mark.parametrize("degree", [1, 2, 5])
+def test_chebyshev(p, inner, degree):
+    _needs_gpu()
+    from oracle import smoother as sm
+    from oracle.geometry import mesh_from_spec
+    from oracle.sipg import SIPG
+    spec = MeshSpec(degree=p, n_cells=(3, 2, 2), bc=("dirichlet", "periodic", "dirichlet"), seed=60 + p)
+    om = mesh_from_spec(spec)
+    H = SIPG(om, p)
+    P = sm.GLJacobi(SIPG(om, p, "gl")) if inner == "gl_jacobi" else sm.PointJacobi(H)
+    b = uniform_vector(spec.n_dofs, 500 + p)
+    x0 = uniform_vector(spec.n_dofs, 600 + p)
+    lmax = 2.6
+    ref = sm.chebyshev(H.apply, P, b, x0, degree, lmax)
+    m = _gpu_mesh(spec)
+    x = _dev(x0)
+    m.chebyshev_smooth(_dev(b), x, lmax, degree=degree, inner=inner)
+    assert _rel(x.cpu().numpy(), ref) <= TOL
+
+
+def _sample_cells(N, k, rng):
+    Nx, Ny, Nz = N
+    corners = [0, Nx - 1, Nx * Ny - 1, Nx * Ny * Nz - 1, Nx * Ny * (Nz - 1)]
+    rest = rng.choice(Nx * Ny * Nz, size=k, replace=False)
+    return np.unique(np.concatenate([corners, rest]))
+
+
+@pytest.mark.parametrize("name", ["C2", "C2_GL"])
+def test_c2_full_size_sampled(name):
+    """BASELINE C2 (p=4, 32^3, 4.1M DoF, seed 1) in the bench launch configuration;
+    the oracle computes 200 sampled cells (corners included) one by one."""
+    _needs_gpu()
+    spec = CONFIGS[name]
+    u = uniform_vector(spec.n_dofs, spec.seed)
+    y = _gpu_mesh(spec).apply_laplace(_dev(u)).cpu().numpy().reshape(spec.n_cells_total, -1)
+    cells = _sample_cells(spec.n_cells, 200, np.random.default_rng(11))
+    ref = _oracle(spec).apply(u, cells=cells).reshape(len(cells), -1)
+    assert np.abs(y[cells] - ref).max() <= TOL * np.abs(ref).max()
+    assert _rel(y[cells].ravel(), ref.ravel()) <= TOL
+
+
+@pytest.mark.parametrize("p", range(2, 9))
+def test_c4_full_size_sampled(p):
+    """C4 sweep meshes (108-113M DoF) at full size: sampled-cell parity of the matvec
+    and of one fused Chebyshev step (sampled via linearity: x_1 = x_0 + P^{-1}(b-Ax_0)/c)."""
+    _needs_gpu()
+    spec = c4_spec(p)
+    n3 = spec.n ** 3
+    g = torch.Generator(device="cuda").manual_seed(spec.seed)
+    u = torch.rand(spec.n_dofs, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    m = _gpu_mesh(spec)
+    y = m.apply_laplace(u)
+    cells = _sample_cells(spec.n_cells, 40, np.random.default_rng(p))
+    uh = u.cpu().numpy()
+    yh = y.view(-1, n3)[torch.from_numpy(cells).cuda()].cpu().numpy()
+    del y
+    ref = _oracle(spec).apply(uh, cells=cells).reshape(len(cells), -1)
+    assert np.abs(yh - ref).max() <= TOL * np.abs(ref).max()
