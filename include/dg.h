@@ -149,6 +149,12 @@ dg_status dg_inverse_diagonal(dg_mesh m, int32_t inner, double* out, void* strea
 dg_status dg_tables_1d(int32_t degree, int32_t basis, double penalty_factor, double* out,
                        int64_t out_len);
 
+/* Machine characterisation (roofline denominators measured on the running GPU):
+ * kind 0: fp64 FMA throughput in TFLOP/s (DFMA chains, 148*8 blocks);
+ * kind 1: streaming copy bandwidth in GB/s (read + write bytes, 2 GiB buffers);
+ * kind 2: streaming read bandwidth in GB/s.  Best of 5 timed launches. */
+dg_status dg_measure_peak(int32_t kind, double* value, void* stream);
+
 /* Number of kernels this library launched since the handle was created. */
 int64_t dg_kernel_launch_count(dg_mesh m);
 

@@ -52,6 +52,7 @@ SYMBOLS = {
     "dg_inverse_diagonal": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                            ctypes.c_void_p]),
     "dg_kernel_launch_count": (ctypes.c_int64, [ctypes.c_void_p]),
+    "dg_measure_peak": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]),
     "dg_tables_1d": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                     ctypes.c_void_p, ctypes.c_int64]),
 }

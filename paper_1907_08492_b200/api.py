@@ -60,6 +60,14 @@ def get_nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def measure_peak(kind: str, stream=None) -> float:
+    """'fp64' -> TFLOP/s of DFMA; 'copy' / 'read' -> GB/s (see dg_measure_peak)."""
+    v = ctypes.c_double()
+    _check(lib().dg_measure_peak({"fp64": 0, "copy": 1, "read": 2}[kind], ctypes.byref(v),
+                                 _stream(stream)), "dg_measure_peak")
+    return v.value
+
+
 def version() -> str:
     return lib().dg_version().decode()
 

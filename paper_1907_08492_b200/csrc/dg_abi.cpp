@@ -347,6 +347,12 @@ dg_status dg_mesh_query(dg_mesh m, int64_t* nl, int64_t* ng, int32_t* zb, int32_
 
 int64_t dg_kernel_launch_count(dg_mesh m) { return m ? m->launches : -1; }
 
+dg_status dg_measure_peak(int32_t kind, double* value, void* stream) {
+  if (!value || kind < 0 || kind > 2) return fail(DG_ERR_PARAM, "bad kind or NULL value");
+  CUDA_TRY(measure_peak(kind, value, (cudaStream_t)stream));
+  return DG_OK;
+}
+
 dg_status dg_tables_1d(int32_t degree, int32_t basis, double pf, double* out, int64_t out_len) {
   if (!out) return fail(DG_ERR_PARAM, "NULL out");
   Tables1D t;

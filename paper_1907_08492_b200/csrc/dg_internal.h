@@ -67,4 +67,6 @@ struct CartDiagParams {
 cudaError_t launch_cart_diag(int n, const CartDiagParams& p, int Nx, int Ny, int nz, int z0,
                              int Nz_global, double* out, cudaStream_t s);
 
+cudaError_t measure_peak(int kind, double* value, cudaStream_t s);
+
 }  // namespace dgb
