@@ -68,6 +68,17 @@ void pack_eo(const double* A, int n, double* out) {
   out[o++] = (n & 1) ? A[mid * n + mid] : 0.0;
 }
 
+double inv3_host(const double* J, double* Ji) {
+  const double a = J[0], b = J[1], c = J[2], d = J[3], e = J[4], f = J[5], g = J[6], h = J[7], i = J[8];
+  const double A = e * i - f * h, B = -(d * i - f * g), C = d * h - e * g;
+  const double det = a * A + b * B + c * C;
+  const double id = 1.0 / det;
+  Ji[0] = A * id; Ji[3] = B * id; Ji[6] = C * id;
+  Ji[1] = -(b * i - c * h) * id; Ji[4] = (a * i - c * g) * id; Ji[7] = -(a * h - b * g) * id;
+  Ji[2] = (b * f - c * e) * id; Ji[5] = -(a * f - c * d) * id; Ji[8] = (a * e - b * d) * id;
+  return det;
+}
+
 void transpose(const double* A, int n, double* At) {
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j) At[j * n + i] = A[i * n + j];
@@ -84,7 +95,13 @@ struct dg_mesh_s {
   int64_t ncells_local = 0, ndofs_local = 0, ndofs_global = 0;
   double h[3] = {0, 0, 0};
   bool cartesian = false;
+  int geom = GEOM_CONST;          // general path geometry storage
   KronParams kp{};
+  QuadParams qp{};
+  GeomArgs ga{};
+  double* d_G = nullptr;          // PER_QPOINT cell tensors
+  double* d_face[3] = {nullptr, nullptr, nullptr};
+  double* d_jinv = nullptr;       // PER_CELL J^-1 + det J (with ghost planes)
   int zlo = ZSRC_MIRROR, zhi = ZSRC_MIRROR;
   // lazily built inverse diagonals
   double* d_dinv_gl = nullptr;
@@ -151,9 +168,21 @@ void diag_variants(const double* L, const double* Nm, const double* Np, int n, i
 
 dg_status build_diag(dg_mesh m, bool gl, double** dst, cudaStream_t s) {
   if (*dst) return DG_OK;
-  if (!m->cartesian)
-    return fail(DG_ERR_UNSUPPORTED, "inverse diagonal: only Cartesian meshes in this build");
   const Tables1D& t = m->tab;
+  if (!m->cartesian) {
+    DiagTables dt{};
+    const int n = m->n;
+    std::memcpy(dt.S, gl ? t.gl_S : t.S, sizeof(double) * n * n);
+    std::memcpy(dt.DS, gl ? t.gl_DS : t.DS, sizeof(double) * n * n);
+    std::memcpy(dt.v[0], gl ? t.gl_v0 : t.v0, sizeof(double) * n);
+    std::memcpy(dt.v[1], gl ? t.gl_v1 : t.v1, sizeof(double) * n);
+    std::memcpy(dt.d[0], gl ? t.gl_d0 : t.d0, sizeof(double) * n);
+    std::memcpy(dt.d[1], gl ? t.gl_d1 : t.d1, sizeof(double) * n);
+    std::memcpy(dt.w, t.wq, sizeof(double) * n);
+    CUDA_TRY(cudaMalloc(dst, sizeof(double) * (size_t)std::max<int64_t>(m->ndofs_local, 1)));
+    return post_launch(m, launch_diag_general(n, m->geom, dt, m->qp, m->ga, grid_args(m, 0, m->nz), 1,
+                                              *dst, s), "diag_general", s);
+  }
   const int n = m->n;
   const double* M = gl ? t.gl_Mhat : t.Mhat;
   const double* L = gl ? t.gl_Lhat : t.Lhat;
@@ -246,19 +275,75 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
   }
   const bool diagonal = L[1] == 0 && L[2] == 0 && L[3] == 0 && L[5] == 0 && L[6] == 0 && L[7] == 0;
   m->cartesian = diagonal && d->deform_amp == 0.0 && d->geometry == DG_GEOM_CONSTANT;
-  for (int k = 0; k < 3; ++k) m->h[k] = L[4 * k] * (d->box_hi[k] - d->box_lo[k]) / m->N[k];
-  if (!m->cartesian) {
+  for (int k = 0; k < 3; ++k) m->h[k] = (d->box_hi[k] - d->box_lo[k]) / m->N[k];
+  m->geom = d->geometry == DG_GEOM_PER_QPOINT ? GEOM_PER_QPOINT
+            : (d->geometry == DG_GEOM_PER_CELL ? GEOM_PER_CELL : GEOM_CONST);
+  if (d->geometry != DG_GEOM_PER_CELL && d->user_inv_jac) {
     delete m;
-    return fail(DG_ERR_UNSUPPORTED,
-                "this build implements the Cartesian constant-geometry path only "
-                "(diagonal linear_map, deform_amp == 0, DG_GEOM_CONSTANT)");
+    return fail(DG_ERR_PARAM, "user_inv_jac requires DG_GEOM_PER_CELL");
   }
-  for (int k = 0; k < 3; ++k)
-    if (!(m->h[k] > 0) || !std::isfinite(m->h[k])) {
-      delete m;
-      return fail(DG_ERR_NUMERIC, "non-positive cell size in direction %d", k);
+  // affine Jacobian of the undeformed map: J_im = L_im h_m
+  double J0[9], Ji0[9];
+  for (int i = 0; i < 3; ++i)
+    for (int k = 0; k < 3; ++k) J0[i * 3 + k] = L[i * 3 + k] * m->h[k];
+  const double det0 = inv3_host(J0, Ji0);
+  if (!(det0 > 0) || !std::isfinite(det0)) {
+    delete m;
+    return fail(DG_ERR_NUMERIC, "det(L diag(h)) = %g <= 0", det0);
+  }
+  const double pen = (double)(n * n) * (d->penalty_factor > 0 ? d->penalty_factor : 1.0);
+  {
+    // general-path parameters (Eqs. (3)-(5))
+    const Tables1D& t = m->tab;
+    QuadParams& qp = m->qp;
+    std::memset(&qp, 0, sizeof qp);
+    double St[kMaxN * kMaxN], Dt[kMaxN * kMaxN];
+    transpose(t.S, n, St);
+    transpose(t.DS, n, Dt);
+    pack_eo(t.S, n, qp.S);
+    pack_eo(t.DS, n, qp.D);
+    pack_eo(St, n, qp.St);
+    pack_eo(Dt, n, qp.Dt);
+    const int NLq = (d->basis == DG_BASIS_HERMITE_LIKE && n > 2) ? 2 : n;
+    for (int sd = 0; sd < 2; ++sd)
+      for (int l = 0; l < NLq; ++l) {
+        const int Lo = sd ? n - NLq + l : l;
+        const int Ln = sd ? l : n - NLq + l;
+        qp.sf[sd][l] = sd ? t.v1[Lo] : t.v0[Lo];
+        qp.df[sd][l] = sd ? t.d1[Lo] : t.d0[Lo];
+        qp.sfn[sd][l] = sd ? t.v0[Ln] : t.v1[Ln];
+        qp.dfn[sd][l] = sd ? t.d0[Ln] : t.d1[Ln];
+      }
+    for (int q = 0; q < n; ++q) qp.w[q] = t.wq[q];
+    // constant geometry: G0 = det J J^-1 J^-T; per direction d, r = row d of J^-1:
+    //   dA_ref J^-1 n_+ = det J J^-1 r,  sigma dA_ref = pen |r| det J |r|
+    qp.G0[0] = det0 * (Ji0[0] * Ji0[0] + Ji0[1] * Ji0[1] + Ji0[2] * Ji0[2]);
+    qp.G0[1] = det0 * (Ji0[3] * Ji0[3] + Ji0[4] * Ji0[4] + Ji0[5] * Ji0[5]);
+    qp.G0[2] = det0 * (Ji0[6] * Ji0[6] + Ji0[7] * Ji0[7] + Ji0[8] * Ji0[8]);
+    qp.G0[3] = det0 * (Ji0[0] * Ji0[3] + Ji0[1] * Ji0[4] + Ji0[2] * Ji0[5]);
+    qp.G0[4] = det0 * (Ji0[0] * Ji0[6] + Ji0[1] * Ji0[7] + Ji0[2] * Ji0[8]);
+    qp.G0[5] = det0 * (Ji0[3] * Ji0[6] + Ji0[4] * Ji0[7] + Ji0[5] * Ji0[8]);
+    for (int dd = 0; dd < 3; ++dd) {
+      const double* r = Ji0 + 3 * dd;
+      const double nr = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+      for (int k = 0; k < 3; ++k)
+        qp.cw0[dd][k] = det0 * (Ji0[k * 3] * r[0] + Ji0[k * 3 + 1] * r[1] + Ji0[k * 3 + 2] * r[2]);
+      qp.sdA0[dd] = pen * nr * det0 * nr;
     }
-
+    double TiT[kMaxN * kMaxN];
+    transpose(t.Tinv, n, TiT);
+    pack_eo(TiT, n, qp.TiT);
+    pack_eo(t.Tinv, n, qp.Ti);
+    m->ga.pen = pen;
+  }
+  if (m->cartesian) {
+    for (int k = 0; k < 3; ++k) m->h[k] = L[4 * k] * (d->box_hi[k] - d->box_lo[k]) / m->N[k];
+    for (int k = 0; k < 3; ++k)
+      if (!(m->h[k] > 0) || !std::isfinite(m->h[k])) {
+        delete m;
+        return fail(DG_ERR_NUMERIC, "non-positive cell size in direction %d", k);
+      }
+  }
   // Kronecker parameters: L_d = (V/h_d^2) Lhat, Nm/Np blocks [NL][NL]
   {
     const Tables1D& t = m->tab;
@@ -314,6 +399,86 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
       return fail(DG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
     }
   }
+  if (m->geom == GEOM_PER_CELL) {
+    const int64_t plane = (int64_t)m->N[0] * m->N[1];
+    const int64_t cnt = plane * (m->nz + 2);
+    std::vector<double> h(cnt * 10);
+    if (d->user_inv_jac && nranks > 1) {
+      dg_mesh_destroy(m);
+      return fail(DG_ERR_UNSUPPORTED, "user_inv_jac with nranks > 1 (ghost-plane exchange) not in this build");
+    }
+    for (int64_t c = 0; c < cnt; ++c) {
+      const int zl = (int)(c / plane) - 1;
+      const int64_t rem = c % plane;
+      double Ji[9];
+      if (d->user_inv_jac) {
+        int zs = zl;
+        if (zs < 0) zs = (d->bc[2] == DG_BC_PERIODIC) ? m->nz - 1 : 0;
+        if (zs >= m->nz) zs = (d->bc[2] == DG_BC_PERIODIC) ? 0 : m->nz - 1;
+        std::memcpy(Ji, d->user_inv_jac + ((int64_t)zs * plane + rem) * 9, sizeof Ji);
+      } else {
+        std::memcpy(Ji, Ji0, sizeof Ji);
+      }
+      double Jm[9];
+      const double dinv = inv3_host(Ji, Jm);      // det(J^-1)
+      const double detJ = 1.0 / dinv;
+      if (!(detJ > 0) || !std::isfinite(detJ)) {
+        dg_mesh_destroy(m);
+        return fail(DG_ERR_NUMERIC, "per-cell det J <= 0 or non-finite at cell %lld", (long long)c);
+      }
+      std::memcpy(&h[c * 10], Ji, sizeof Ji);
+      h[c * 10 + 9] = detJ;
+    }
+    cudaError_t e1 = cudaMalloc(&m->d_jinv, sizeof(double) * h.size());
+    if (e1 == cudaSuccess)
+      e1 = cudaMemcpyAsync(m->d_jinv, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s);
+    if (e1 == cudaSuccess) e1 = cudaStreamSynchronize(s);
+    if (e1 != cudaSuccess) {
+      dg_mesh_destroy(m);
+      return fail(DG_ERR_CUDA, "per-cell geometry: %s", cudaGetErrorString(e1));
+    }
+    m->ga.jinv = m->d_jinv;
+  } else if (m->geom == GEOM_PER_QPOINT) {
+    const int64_t n3 = (int64_t)n * n * n;
+    MapParams mp{};
+    for (int k = 0; k < 9; ++k) mp.L[k] = L[k];
+    for (int k = 0; k < 3; ++k) {
+      mp.h[k] = m->h[k];
+      mp.Nglob[k] = m->N[k];
+      mp.bc[k] = d->bc[k];
+    }
+    mp.amp = d->deform_amp;
+    mp.z0 = m->z_begin;
+    mp.pen = pen;
+    for (int q = 0; q < n; ++q) {
+      mp.xq[q] = m->tab.xq[q];
+      mp.wq[q] = m->tab.wq[q];
+    }
+    const int Nx = m->N[0], Ny = m->N[1], nz = m->nz;
+    size_t fcount[3] = {(size_t)(Nx + 1) * Ny * nz, (size_t)Nx * (Ny + 1) * nz, (size_t)Nx * Ny * (nz + 1)};
+    int* d_err = nullptr;
+    cudaError_t e1 = cudaMalloc(&m->d_G, sizeof(double) * (size_t)(m->ncells_local * 6 * n3));
+    for (int k = 0; k < 3 && e1 == cudaSuccess; ++k)
+      e1 = cudaMalloc(&m->d_face[k], sizeof(double) * fcount[k] * 4 * n * n);
+    if (e1 == cudaSuccess) e1 = cudaMalloc(&d_err, sizeof(int));
+    if (e1 == cudaSuccess) e1 = cudaMemsetAsync(d_err, 0, sizeof(int), s);
+    if (e1 == cudaSuccess) e1 = launch_geom_qpoint(n, mp, Nx, Ny, nz, m->d_G, m->d_face, d_err, s);
+    int herr = 0;
+    if (e1 == cudaSuccess) e1 = cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e1 == cudaSuccess) e1 = cudaStreamSynchronize(s);
+    cudaFree(d_err);
+    m->launches += 5;
+    if (e1 != cudaSuccess) {
+      dg_mesh_destroy(m);
+      return fail(DG_ERR_CUDA, "per-q-point geometry: %s", cudaGetErrorString(e1));
+    }
+    if (herr) {
+      dg_mesh_destroy(m);
+      return fail(DG_ERR_NUMERIC, "det J <= 0 or non-finite at some quadrature point");
+    }
+    m->ga.G = m->d_G;
+    for (int k = 0; k < 3; ++k) m->ga.face[k] = m->d_face[k];
+  }
   cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
     dg_mesh_destroy(m);
@@ -325,6 +490,9 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
 
 dg_status dg_mesh_destroy(dg_mesh m) {
   if (!m) return DG_OK;
+  cudaFree(m->d_G);
+  for (int d = 0; d < 3; ++d) cudaFree(m->d_face[d]);
+  cudaFree(m->d_jinv);
   cudaFree(m->d_dinv_gl);
   cudaFree(m->d_dinv_pj);
   cudaFree(m->d_recv_lo);
@@ -378,8 +546,6 @@ dg_status dg_apply_laplace(dg_mesh m, const double* u, double* y, int32_t flags,
   if (!m || !u || !y) return fail(DG_ERR_PARAM, "NULL argument");
   if (u == y) return fail(DG_ERR_PARAM, "u and y alias");
   if (flags & ~(DG_APPLY_HALO_READY | DG_APPLY_QUADRATURE)) return fail(DG_ERR_PARAM, "bad flags");
-  if (flags & DG_APPLY_QUADRATURE)
-    return fail(DG_ERR_UNSUPPORTED, "quadrature kernel not in this build");
   cudaStream_t s = (cudaStream_t)stream;
   if (!(flags & DG_APPLY_HALO_READY)) {
     dg_status st = halo_exchange_impl(m, u, s);
@@ -387,7 +553,10 @@ dg_status dg_apply_laplace(dg_mesh m, const double* u, double* y, int32_t flags,
   }
   ChebyArgs ch{};
   GridArgs g = grid_args(m, 0, m->nz);
-  return post_launch(m, launch_kron(m->n, m->NL, KMODE_APPLY, m->kp, g, u, y, ch, s), "kron_apply", s);
+  if (m->cartesian && !(flags & DG_APPLY_QUADRATURE))
+    return post_launch(m, launch_kron(m->n, m->NL, KMODE_APPLY, m->kp, g, u, y, ch, s), "kron_apply", s);
+  return post_launch(m, launch_quad(m->n, m->NL, m->geom, KMODE_APPLY, m->qp, m->ga, g, u, y, ch, s),
+                     "quad_apply", s);
 }
 
 dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, void* stream) {
@@ -482,7 +651,11 @@ dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* wor
     st = halo_exchange_impl(m, uj, s);
     if (st != DG_OK) return st;
     GridArgs g = grid_args(m, 0, m->nz);
-    st = post_launch(m, launch_kron(m->n, m->NL, mode, m->kp, g, uj, nullptr, ch, s), "kron_cheby", s);
+    if (m->cartesian)
+      st = post_launch(m, launch_kron(m->n, m->NL, mode, m->kp, g, uj, nullptr, ch, s), "kron_cheby", s);
+    else
+      st = post_launch(m, launch_quad(m->n, m->NL, m->geom, mode, m->qp, m->ga, g, uj, nullptr, ch, s),
+                       "quad_cheby", s);
     if (st != DG_OK) return st;
   }
   if (where[degree] != 0)

@@ -52,6 +52,48 @@ struct BchgParams {
   double B[kEO];              // even-odd packed 1D matrix, parity +1
 };
 
+// Kernel parameters of the general quadrature path (Eqs. (3)-(5)):
+// 1D tables in even-odd form, face traces restricted to the NL layers next to a
+// face, and the constant-geometry data (DG_GEOM_CONSTANT).
+struct QuadParams {
+  double S[kEO];               // S[q][j] = phi_j(xq_q), parity +1
+  double D[kEO];               // DS[q][j] = phi_j'(xq_q), parity -1
+  double St[kEO];              // S^T
+  double Dt[kEO];              // DS^T
+  double sf[2][kMaxN];         // own trace  phi_L(s),  L = s ? n-NL+l : l
+  double df[2][kMaxN];         // own trace  phi_L'(s)
+  double sfn[2][kMaxN];        // neighbour trace phi_L(1-s), L = s ? l : n-NL+l
+  double dfn[2][kMaxN];        // neighbour trace phi_L'(1-s)
+  double w[kMaxN];             // Gauss weights on (0,1)
+  double G0[6];                // CONSTANT: det J J^-1 J^-T  (xx, yy, zz, xy, xz, yz)
+  double cw0[3][3];            // CONSTANT: det J |J^-T e_d| J^-1 n_+(d)   (times w_a w_b)
+  double sdA0[3];              // CONSTANT: sigma_d det J |J^-T e_d|        (times w_a w_b)
+  double TiT[kEO];             // T^{-T}
+  double Ti[kEO];              // T^{-1}
+};
+
+enum { GEOM_CONST = 0, GEOM_PER_CELL = 1, GEOM_PER_QPOINT = 2 };
+
+// Geometry arrays of the general path (device pointers, library-owned).
+struct GeomArgs {
+  const double* G;             // PER_QPOINT: [cell][6][n^3]  w_q det J J^-1 J^-T
+  const double* face[3];       // PER_QPOINT: per direction [face][4][n^2]: dA J^-1 n_+ (3), sigma dA
+  const double* jinv;          // PER_CELL:  [cell][10]: J^-1 (row-major), det J
+  double pen;                  // (p+1)^2 * penalty_factor  (PER_CELL)
+};
+
+// Analytic mesh map: x = L X + amp s(Xh), X = lo + (c+xi) h.
+struct MapParams {
+  double L[9];
+  double h[3];
+  double amp;
+  int Nglob[3];
+  int z0;                      // global index of local plane 0
+  int bc[3];
+  double pen;                  // (p+1)^2 * penalty_factor
+  double xq[kMaxN], wq[kMaxN];
+};
+
 // Launchers (k_kron.cu, k_basis_change.cu, k_setup.cu)
 cudaError_t launch_kron(int n, int NL, int mode, const KronParams& kp, const GridArgs& g,
                         const double* u, double* y, const ChebyArgs& ch, cudaStream_t s);
@@ -68,5 +110,20 @@ cudaError_t launch_cart_diag(int n, const CartDiagParams& p, int Nx, int Ny, int
                              int Nz_global, double* out, cudaStream_t s);
 
 cudaError_t measure_peak(int kind, double* value, cudaStream_t s);
+
+// general quadrature path (k_quad.cu) and its setup (k_geom.cu)
+cudaError_t launch_quad(int n, int NL, int geom, int mode, const QuadParams& qp, const GeomArgs& ga,
+                        const GridArgs& g, const double* u, double* y, const ChebyArgs& ch,
+                        cudaStream_t s);
+cudaError_t launch_geom_qpoint(int n, const MapParams& mp, int Nx, int Ny, int nz, double* G,
+                               double* face[3], int* err_flag, cudaStream_t s);
+// diagonal of the operator in a basis given by tables (S, DS, v0, v1, d0, d1 at the
+// Gauss points), any geometry; invert -> 1/diag
+struct DiagTables {
+  double S[kMaxN * kMaxN], DS[kMaxN * kMaxN], v[2][kMaxN], d[2][kMaxN], w[kMaxN];
+};
+cudaError_t launch_diag_general(int n, int geom, const DiagTables& t, const QuadParams& qp,
+                                const GeomArgs& ga, const GridArgs& g, int invert, double* out,
+                                cudaStream_t s);
 
 }  // namespace dgb

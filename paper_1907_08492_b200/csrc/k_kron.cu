@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "dg_internal.h"
+#include "loader.cuh"
 
 namespace dgb {
 namespace {
@@ -39,12 +40,6 @@ struct KLayout {
 
 template <int N>
 __device__ __forceinline__ int64_t cell_off(int64_t c) { return c * (int64_t)(N * N * N); }
-
-// index of (d-coordinate m, tangential a, b) inside a cell, for a face normal to d
-template <int N>
-__device__ __forceinline__ int face_idx(int d, int m, int a, int b) {
-  return d == 0 ? (b * N + a) * N + m : (d == 1 ? (b * N + m) * N + a : (m * N + b) * N + a);
-}
 
 template <int N, int NL, int CPB, int MODE>
 __global__ void __launch_bounds__(CPB * N * N)
@@ -63,60 +58,6 @@ k_kron(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g
   const int tid = threadIdx.x;
 
   // ---------------------------------------------------------------- P0: loads
-  // own coefficients (contiguous range, coalesced)
-  {
-    const double* src = u + cell_off<N>(cell0);
-    const int total = ncell * N * NN;
-    for (int e = tid; e < total; e += CPB * NN) {
-      const int c = e / (N * NN), r = e % (N * NN);
-      const int k = r / NN, j = (r / N) % N, i = r % N;
-      smem[c * Lay::PER_CELL + (k * N + j) * P + i] = __ldg(src + e);
-    }
-  }
-  // neighbour layers of the 6 faces: NL layers each (2 for Hermite-like)
-  {
-    constexpr int PERC = 6 * NL * NN;
-    const int total = ncell * PERC;
-    for (int e = tid; e < total; e += CPB * NN) {
-      const int c = e / PERC;
-      int r = e % PERC;
-      const int f = r / (NL * NN);
-      r %= NL * NN;
-      const int l = r / NN, b = (r / N) % N, a = r % N;
-      const int d = f >> 1, s = f & 1;
-      const int64_t cid = cell0 + c;
-      const int cx = (int)(cid % g.Nx), cy = (int)((cid / g.Nx) % g.Ny), cz = (int)(cid / plane);
-      const int cd = d == 0 ? cx : (d == 1 ? cy : cz);
-      const int Nd = d == 0 ? g.Nx : (d == 1 ? g.Ny : g.nz);
-      const int L = s == 0 ? N - NL + l : l;                 // neighbour's layer index
-      int nb = cd + (s ? 1 : -1);
-      double v;
-      bool mirror = false, halo = false;
-      if (nb < 0 || nb >= Nd) {
-        if (d < 2) {
-          if (g.bc[d] == DG_BC_PERIODIC) nb = (nb + Nd) % Nd; else mirror = true;
-        } else {
-          const int src = s == 0 ? g.zlo : g.zhi;
-          if (src == ZSRC_LOCAL) nb = (nb + Nd) % Nd;
-          else if (src == ZSRC_MIRROR) mirror = true;
-          else halo = true;
-        }
-      }
-      if (mirror) {
-        v = -__ldg(u + cell_off<N>(cid) + face_idx<N>(d, N - 1 - L, a, b));
-      } else if (halo) {
-        const int cxy = cx + g.Nx * cy;
-        const double* hb = s == 0 ? g.halo_lo : g.halo_hi;
-        v = __ldg(hb + ((int64_t)cxy * NL + l) * NN + b * N + a);
-      } else {
-        const int64_t ncid = ((int64_t)(d == 2 ? nb : cz) * g.Ny + (d == 1 ? nb : cy)) * g.Nx + (d == 0 ? nb : cx);
-        v = __ldg(u + cell_off<N>(ncid) + face_idx<N>(d, L, a, b));
-      }
-      smem[c * Lay::PER_CELL + 3 * Lay::FIELD + f * Lay::FACE + (l * N + b) * P + a] = v;
-    }
-  }
-  __syncthreads();
-
   const int cslot = tid / NN;
   const int line = tid % NN;
   const bool active = cslot < ncell;
@@ -124,6 +65,8 @@ k_kron(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g
   double* F1 = F0 + Lay::FIELD;                      // t, later c
   double* F2 = F1 + Lay::FIELD;                      // a
   double* FC = F2 + Lay::FIELD;                      // 6 faces
+  if (active) stage_cell<N, NL, P, Lay::FACE>(g, u, cell0 + cslot, line, F0, FC);
+  __syncthreads();
 
   // ---------------------------------------------------------------- P1: x-lines
   if (active) {
