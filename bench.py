@@ -31,7 +31,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synthetic import c4_spec  # noqa: E402
+from synthetic import CONFIGS, c4_spec  # noqa: E402
 
 METRIC = "SIPG Laplace matvec DoF/s (fp64) and achieved HBM GB/s vs peak, p=2..8"
 UNIT = "DoF/s"
@@ -45,6 +45,8 @@ def args_():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--degrees", default="2,3,4,5,6,7,8")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c2", "c3", "c5"],
+                    help="c4: degree sweep (default, the metric's configuration); c2/c3/c5: other BASELINE configs")
     ap.add_argument("--cheby-degree", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -224,13 +226,42 @@ def lanczos_lambda_max(m, iters=15):
     return float(np.linalg.eigvalsh(T)[-1])
 
 
+def workload_specs(a):
+    if a.workload == "c4":
+        return [c4_spec(int(x)) for x in a.degrees.split(",")]
+    if a.workload == "c2":
+        return [CONFIGS["C2"], CONFIGS["C2_GL"]]
+    if a.workload == "c3":
+        return [CONFIGS["C3"]]
+    return [CONFIGS["C5"]]
+
+
+def geometry_bytes_per_dof(spec):
+    """Algorithmic geometry bytes per DoF read by one operator pass (each datum once):
+    per-q-point merged tensor 6 words/q-point + per face point 4 words (3 faces per cell)."""
+    if spec.geometry != "per_qpoint":
+        return 0.0
+    n = spec.n
+    return 6 * 8 + 3 * 4 * 8 * n * n / n ** 3
+
+
+WORKLOAD_TEXT = {
+    "c4": "C4 degree sweep p=2..8, N_p=round(480/(p+1)) cells per direction, matvec + H->GL basis change "
+          "+ degree-5 Chebyshev (GL-Jacobi) per degree",
+    "c2": "C2 p=4 32^3 Cartesian, Hermite-like vs nodal Gauss-Lobatto (full-neighbour reads)",
+    "c3": "C3 p=5 48^3 curved (amp 0.05), per-quadrature-point geometry, general quadrature kernel",
+    "c5": "C5 p=5 128^3 Cartesian (453M DoF), z-slabs",
+}
+
+
 def run_ours(a, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     import paper_1907_08492_b200 as P
 
-    degrees = [int(x) for x in a.degrees.split(",")]
+    specs = workload_specs(a)
+    degrees = [sp.degree for sp in specs]
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
@@ -253,8 +284,8 @@ def run_ours(a, rank, world, local_rank):
         fp64_peak = P.measure_peak("fp64")
     # ---------------------------------------------------------------- setup per degree
     setups = []
-    for p in degrees:
-        spec = c4_spec(p)
+    for spec in specs:
+        p = spec.degree
         nccl_id = None
         if world > 1:
             obj = [P.get_nccl_unique_id() if rank == 0 else None]
@@ -273,7 +304,8 @@ def run_ours(a, rank, world, local_rank):
         work2 = torch.empty(2 * nl, dtype=torch.float64, device=dev)
         lmax = lanczos_lambda_max(m)
         setups.append(dict(p=p, spec=spec, m=m, u=u, b=b, x=x, y=y, v=v, work2=work2, lmax=lmax,
-                           n_global=m.n_global_dofs))
+                           n_global=m.n_global_dofs, key=f"p{p}" + ("-gl" if spec.basis == "gl" else "")
+                           + ("-curved" if spec.deform_amp else "")))
     torch.cuda.synchronize()
 
     def step(record):
@@ -284,7 +316,8 @@ def run_ours(a, rank, world, local_rank):
             s["m"].apply_laplace(s["u"], s["y"])
             if record:
                 ev[1].record(stream)
-            s["m"].basis_change("T", s["u"], s["v"])
+            if s["spec"].basis == "hermite":
+                s["m"].basis_change("T", s["u"], s["v"])
             if record:
                 ev[2].record(stream)
             s["m"].chebyshev_smooth(s["b"], s["x"], s["lmax"], degree=a.cheby_degree, work2=s["work2"])
@@ -318,25 +351,30 @@ def run_ours(a, rank, world, local_rank):
         nd = s["n_global"]
         K = a.steps
         cd = a.cheby_degree
-        ch_bytes = nd * (BYTES_PER_DOF["cheby_first"] + (cd - 1) * BYTES_PER_DOF["cheby"])
-        ops[f"p{s['p']}"] = {
+        gb = geometry_bytes_per_dof(s["spec"])
+        ch_bytes = nd * (BYTES_PER_DOF["cheby_first"] + (cd - 1) * BYTES_PER_DOF["cheby"] + cd * gb)
+        mv_bytes = nd * (BYTES_PER_DOF["matvec"] + gb)
+        ops[s["key"]] = {
             "n_dofs": nd, "lambda_max": s["lmax"],
             "matvec_dofs_per_s": nd * K / (mv * 1e-3),
-            "matvec_gbs": nd * BYTES_PER_DOF["matvec"] * K / (mv * 1e-3) / 1e9,
-            "basis_change_dofs_per_s": nd * K / (bc * 1e-3),
-            "basis_change_gbs": nd * BYTES_PER_DOF["basis_change"] * K / (bc * 1e-3) / 1e9,
+            "matvec_gbs": mv_bytes * K / (mv * 1e-3) / 1e9,
+            "matvec_bytes_per_dof": mv_bytes / nd,
+            "basis_change_dofs_per_s": nd * K / (bc * 1e-3) if bc > 1e-3 else None,
+            "basis_change_gbs": nd * BYTES_PER_DOF["basis_change"] * K / (bc * 1e-3) / 1e9 if bc > 1e-3 else None,
             "cheby_step_dofs_per_s": nd * cd * K / (ch * 1e-3),
             "cheby_sweep_gbs": ch_bytes * K / (ch * 1e-3) / 1e9,
         }
-        dom["matvec"][0] += nd * BYTES_PER_DOF["matvec"] * K
+        dom["matvec"][0] += mv_bytes * K
         dom["matvec"][1] += mv
-        dom["basis_change"][0] += nd * BYTES_PER_DOF["basis_change"] * K
-        dom["basis_change"][1] += bc
+        if bc > 1e-3:
+            dom["basis_change"][0] += nd * BYTES_PER_DOF["basis_change"] * K
+            dom["basis_change"][1] += bc
         dom["chebyshev_step"][0] += ch_bytes * K
         dom["chebyshev_step"][1] += ch
     n_sum = sum(s["n_global"] for s in setups)
     value = n_sum * a.steps / (t_mv_sum * 1e-3)
     dom_name = max(dom, key=lambda k: dom[k][1])
+    dom = {k: v if v[1] > 0 else [0.0, 1e-30] for k, v in dom.items()}
     ach = dom[dom_name][0] / (dom[dom_name][1] * 1e-3) / 1e9 / world   # per-GPU GB/s
     roofline = {"bound": "hbm", "kernel": {"matvec": "k_kron<APPLY>", "basis_change": "k_bchg",
                                            "chebyshev_step": "k_kron<CHEBY_GL>"}[dom_name],
@@ -352,8 +390,7 @@ def run_ours(a, rank, world, local_rank):
             "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded uniform[-1,1) fp64 vectors on Cartesian [0,1]^3 meshes (mirror Dirichlet)",
-            "config": {"workload": "C4 degree sweep p=2..8, N_p=round(480/(p+1)) cells per direction, "
-                                   "matvec + H->GL basis change + degree-5 Chebyshev (GL-Jacobi) per degree",
+            "config": {"workload": WORKLOAD_TEXT[a.workload],
                        "degrees": degrees, "n_dofs_total": n_sum,
                        "l2_flush": "inputs larger than L2 (0.87-0.90 GB per vector >> 126 MB)",
                        "parallelism": f"z-slab x{world}"},
@@ -388,7 +425,7 @@ def run_ours(a, rank, world, local_rank):
     if rank == 0 and world == 1 and not a.no_cpu_baseline and not a.quick:
         dofs = secs = 0.0
         cells = {}
-        for p in degrees:
+        for p in sorted(set(degrees)):
             r, c, t = oracle_rate(p, 3.0)
             dofs += r * t
             secs += t

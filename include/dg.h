@@ -91,7 +91,9 @@ typedef struct {
   int32_t rank, nranks;    /* z-slab decomposition: rank r owns planes
                               [r*Nz/nranks, (r+1)*Nz/nranks)                                */
   const void* nccl_unique_id; /* 128 bytes from dg_get_nccl_unique_id on rank 0, broadcast
-                                 by the caller; NULL when nranks == 1                       */
+                                 by the caller; NULL when nranks == 1, or NULL with
+                                 nranks > 1 for an external halo transport
+                                 (dg_halo_pack / dg_halo_set)                               */
   void*   stream;          /* cudaStream_t for setup work (NULL = default)                 */
 } dg_mesh_desc;
 
@@ -114,6 +116,29 @@ dg_status dg_mesh_destroy(dg_mesh m);
 /* Sizes of the local slab: owned DoFs, global DoFs, owned planes [z_begin, z_end). */
 dg_status dg_mesh_query(dg_mesh m, int64_t* n_local_dofs, int64_t* n_global_dofs,
                         int32_t* z_begin, int32_t* z_end);
+
+/* Host-only slab plan for z-slab decomposition (no GPU needed):
+ * out[0] = z_begin, out[1] = z_end (owned planes [z_begin, z_end) = [r*Nz/P, (r+1)*Nz/P)),
+ * out[2] = lower peer rank (-1: mirror boundary, rank itself never), out[3] = upper peer,
+ * out[4] = NL (layers per halo plane: 2 Hermite-like (p>=2), n otherwise).
+ * Message order of one exchange (both directions, grouped): first "up"  (send the top
+ * NL layers of the top plane to the upper peer, receive the lower peer's into recv_lo),
+ * then "down" (send the bottom NL layers of the bottom plane to the lower peer, receive
+ * the upper peer's into recv_hi).  Halo layout: [cx + Nx*cy][l][j][i]. */
+dg_status dg_slab_plan(int32_t Nz, int32_t nranks, int32_t rank, int32_t bc_z, int32_t degree,
+                       int32_t basis, int32_t* out6);
+
+/* Halo buffers with an external transport (NCCL-free; e.g. one-GPU loopback tests):
+ * dg_halo_pack writes the two send planes of u (device, count doubles each, count from
+ * dg_mesh_query_halo); dg_halo_set installs received planes (device) as the halo.
+ * Meshes built with nranks > 1 and nccl_unique_id == NULL use this external mode. */
+/* Host-only reference packer (no GPU): the two send planes of a host slab u_slab
+ * (nz local planes of Nx*Ny cells), same index map as the device pack kernel. */
+dg_status dg_halo_pack_host(const double* u_slab, int32_t degree, int32_t basis, int32_t Nx,
+                            int32_t Ny, int32_t nz, double* send_lo, double* send_hi);
+dg_status dg_mesh_query_halo(dg_mesh m, int64_t* count, int32_t* lo_peer, int32_t* hi_peer);
+dg_status dg_halo_pack(dg_mesh m, const double* u, double* send_lo, double* send_hi, void* stream);
+dg_status dg_halo_set(dg_mesh m, const double* recv_lo, const double* recv_hi, void* stream);
 
 /* Fill the library-owned z-halo of u: the two Hermite face layers (all n layers for
  * the GL basis) of the neighbouring ranks' boundary planes, via grouped ncclSend/

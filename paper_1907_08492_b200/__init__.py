@@ -7,4 +7,5 @@ it has not been built (`python -m paper_1907_08492_b200.build`).
 """
 from ._lib import LIB_PATH, lib  # noqa: F401
 from .api import (APPLY_HALO_READY, APPLY_QUADRATURE, DgError, Mesh, get_nccl_unique_id,  # noqa: F401
-                  measure_peak, mesh_from_spec, tables_1d, version)
+                  halo_pack_host, measure_peak, mesh_from_spec, slab_plan, tables_1d,
+                  version)

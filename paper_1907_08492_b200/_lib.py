@@ -53,6 +53,13 @@ SYMBOLS = {
                                            ctypes.c_void_p]),
     "dg_kernel_launch_count": (ctypes.c_int64, [ctypes.c_void_p]),
     "dg_measure_peak": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]),
+    "dg_slab_plan": (ctypes.c_int, [ctypes.c_int32] * 6 + [ctypes.POINTER(ctypes.c_int32)]),
+    "dg_halo_pack_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]),
+    "dg_mesh_query_halo": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                          ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
+    "dg_halo_pack": (ctypes.c_int, [ctypes.c_void_p] * 5),
+    "dg_halo_set": (ctypes.c_int, [ctypes.c_void_p] * 4),
     "dg_tables_1d": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                     ctypes.c_void_p, ctypes.c_int64]),
 }

@@ -91,6 +91,28 @@ def tables_1d(degree: int, basis: str = "hermite", penalty_factor: float = 1.0):
     return res
 
 
+def slab_plan(Nz, nranks, rank, bc_z="dirichlet", degree=3, basis="hermite"):
+    """Host-only dg_slab_plan: dict(z_begin, z_end, lo_peer, hi_peer, NL)."""
+    out = (ctypes.c_int32 * 6)()
+    _check(lib().dg_slab_plan(int(Nz), int(nranks), int(rank), BC[bc_z], int(degree), BASIS[basis], out),
+           "dg_slab_plan")
+    return dict(z_begin=out[0], z_end=out[1], lo_peer=out[2], hi_peer=out[3], NL=out[4])
+
+
+def halo_pack_host(u_slab, degree, basis, Nx, Ny, nz):
+    """Host-only reference packer: (send_lo, send_hi) numpy arrays of a host slab."""
+    import numpy as np
+    u = np.ascontiguousarray(u_slab, dtype=np.float64)
+    n = degree + 1
+    NL = 2 if (basis == "hermite" and degree >= 2) else n
+    cnt = Nx * Ny * NL * n * n
+    lo = np.empty(cnt)
+    hi = np.empty(cnt)
+    _check(lib().dg_halo_pack_host(u.ctypes.data, degree, BASIS[basis], Nx, Ny, nz, lo.ctypes.data,
+                                   hi.ctypes.data), "dg_halo_pack_host")
+    return lo, hi
+
+
 class Mesh:
     """dg_mesh_setup(...) handle.  All vectors are CUDA float64 tensors of n_local_dofs."""
 
@@ -161,6 +183,29 @@ class Mesh:
     def halo_exchange(self, u, stream=None):
         _check(lib().dg_halo_exchange(self._h, _ptr(u, self.n_local_dofs, "u"), _stream(stream)),
                "dg_halo_exchange")
+
+    def query_halo(self):
+        c, lo, hi = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().dg_mesh_query_halo(self._h, ctypes.byref(c), ctypes.byref(lo), ctypes.byref(hi)),
+               "dg_mesh_query_halo")
+        return dict(count=c.value, lo_peer=lo.value, hi_peer=hi.value)
+
+    def halo_pack(self, u, send_lo=None, send_hi=None, stream=None):
+        """External transport: the two send planes of u (device tensors)."""
+        cnt = self.query_halo()["count"]
+        if send_lo is None:
+            send_lo = torch.empty(max(cnt, 1), dtype=torch.float64, device="cuda")
+        if send_hi is None:
+            send_hi = torch.empty(max(cnt, 1), dtype=torch.float64, device="cuda")
+        _check(lib().dg_halo_pack(self._h, _ptr(u, self.n_local_dofs, "u"), _ptr(send_lo, cnt, "send_lo"),
+                                  _ptr(send_hi, cnt, "send_hi"), _stream(stream)), "dg_halo_pack")
+        return send_lo, send_hi
+
+    def halo_set(self, recv_lo=None, recv_hi=None, stream=None):
+        cnt = self.query_halo()["count"]
+        lo = _ptr(recv_lo, cnt, "recv_lo") if recv_lo is not None else ctypes.c_void_p(0)
+        hi = _ptr(recv_hi, cnt, "recv_hi") if recv_hi is not None else ctypes.c_void_p(0)
+        _check(lib().dg_halo_set(self._h, lo, hi, _stream(stream)), "dg_halo_set")
 
     def apply_laplace(self, u, y=None, flags=0, stream=None):
         if y is None:

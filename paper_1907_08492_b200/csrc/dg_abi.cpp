@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "dg_internal.h"
+#include "halo_index.h"
 
 using namespace dgb;
 
@@ -113,6 +114,10 @@ struct dg_mesh_s {
   double* d_send_hi = nullptr;
   int64_t halo_count = 0;         // doubles per halo buffer
   ncclComm_t comm = nullptr;
+  bool external = false;          // nranks > 1 without NCCL: dg_halo_pack / dg_halo_set
+  int lo_peer = -1, hi_peer = -1;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   int rank = 0, nranks = 1;
   int64_t launches = 0;
 };
@@ -204,6 +209,17 @@ dg_status build_diag(dg_mesh m, bool gl, double** dst, cudaStream_t s) {
 }
 
 dg_status halo_exchange_impl(dg_mesh m, const double* u, cudaStream_t s);
+dg_status run_pass(dg_mesh m, int mode, bool kron, const double* u, double* y, const ChebyArgs& ch,
+                   bool halo_ready, cudaStream_t s);
+
+// z-slab partition and peers (shared by dg_slab_plan and dg_mesh_setup)
+void slab_plan(int Nz, int P, int r, int bcz, int out[4]) {
+  out[0] = (int)((int64_t)r * Nz / P);
+  out[1] = (int)((int64_t)(r + 1) * Nz / P);
+  const bool per = bcz == DG_BC_PERIODIC;
+  out[2] = P == 1 ? -1 : (r > 0 ? r - 1 : (per ? P - 1 : -1));
+  out[3] = P == 1 ? -1 : (r < P - 1 ? r + 1 : (per ? 0 : -1));
+}
 
 }  // namespace
 
@@ -241,7 +257,6 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
   const int nranks = d->nranks < 1 ? 1 : d->nranks;
   if (d->rank < 0 || d->rank >= nranks) return fail(DG_ERR_PARAM, "rank %d of %d", d->rank, nranks);
   if (d->n_cells[2] < nranks) return fail(DG_ERR_PARAM, "Nz=%d < nranks=%d", d->n_cells[2], nranks);
-  if (nranks > 1 && !d->nccl_unique_id) return fail(DG_ERR_PARAM, "nranks > 1 needs nccl_unique_id");
 
   dg_mesh m = new dg_mesh_s();
   m->desc = *d;
@@ -255,8 +270,14 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
   const int n = m->n = d->degree + 1;
   m->NL = (d->basis == DG_BASIS_HERMITE_LIKE && n > 2) ? 2 : n;
   for (int k = 0; k < 3; ++k) m->N[k] = d->n_cells[k];
-  m->z_begin = (int)((int64_t)d->rank * m->N[2] / nranks);
-  m->z_end = (int)((int64_t)(d->rank + 1) * m->N[2] / nranks);
+  {
+    int plan[4];
+    slab_plan(m->N[2], nranks, d->rank, d->bc[2], plan);
+    m->z_begin = plan[0];
+    m->z_end = plan[1];
+    m->lo_peer = plan[2];
+    m->hi_peer = plan[3];
+  }
   m->nz = m->z_end - m->z_begin;
   const int64_t n3 = (int64_t)n * n * n;
   m->ncells_local = (int64_t)m->N[0] * m->N[1] * m->nz;
@@ -374,8 +395,8 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
   if (nranks == 1) {
     m->zlo = m->zhi = zper ? ZSRC_LOCAL : ZSRC_MIRROR;
   } else {
-    m->zlo = (d->rank == 0 && !zper) ? ZSRC_MIRROR : ZSRC_HALO;
-    m->zhi = (d->rank == nranks - 1 && !zper) ? ZSRC_MIRROR : ZSRC_HALO;
+    m->zlo = m->lo_peer >= 0 ? ZSRC_HALO : ZSRC_MIRROR;
+    m->zhi = m->hi_peer >= 0 ? ZSRC_HALO : ZSRC_MIRROR;
   }
   cudaStream_t s = (cudaStream_t)d->stream;
   if (m->zlo == ZSRC_HALO || m->zhi == ZSRC_HALO) {
@@ -390,13 +411,26 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
       dg_mesh_destroy(m);
       return fail(DG_ERR_CUDA, "halo alloc: %s", cudaGetErrorString(e));
     }
-    ncclUniqueId id;
-    std::memcpy(&id, d->nccl_unique_id, sizeof id);
-    ncclResult_t r = ncclCommInitRank(&m->comm, nranks, id, d->rank);
-    if (r != ncclSuccess) {
-      m->comm = nullptr;
-      dg_mesh_destroy(m);
-      return fail(DG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    cudaMemsetAsync(m->d_recv_lo, 0, bytes, s);
+    cudaMemsetAsync(m->d_recv_hi, 0, bytes, s);
+    if (d->nccl_unique_id) {
+      ncclUniqueId id;
+      std::memcpy(&id, d->nccl_unique_id, sizeof id);
+      ncclResult_t r = ncclCommInitRank(&m->comm, nranks, id, d->rank);
+      if (r != ncclSuccess) {
+        m->comm = nullptr;
+        dg_mesh_destroy(m);
+        return fail(DG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+      }
+      cudaError_t ce = cudaStreamCreateWithFlags(&m->comm_stream, cudaStreamNonBlocking);
+      if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&m->ev_ready, cudaEventDisableTiming);
+      if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&m->ev_halo, cudaEventDisableTiming);
+      if (ce != cudaSuccess) {
+        dg_mesh_destroy(m);
+        return fail(DG_ERR_CUDA, "comm stream/events: %s", cudaGetErrorString(ce));
+      }
+    } else {
+      m->external = true;
     }
   }
   if (m->geom == GEOM_PER_CELL) {
@@ -500,6 +534,9 @@ dg_status dg_mesh_destroy(dg_mesh m) {
   cudaFree(m->d_send_lo);
   cudaFree(m->d_send_hi);
   if (m->comm) ncclCommDestroy(m->comm);
+  if (m->ev_ready) cudaEventDestroy(m->ev_ready);
+  if (m->ev_halo) cudaEventDestroy(m->ev_halo);
+  if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
   delete m;
   return DG_OK;
 }
@@ -514,6 +551,59 @@ dg_status dg_mesh_query(dg_mesh m, int64_t* nl, int64_t* ng, int32_t* zb, int32_
 }
 
 int64_t dg_kernel_launch_count(dg_mesh m) { return m ? m->launches : -1; }
+
+dg_status dg_slab_plan(int32_t Nz, int32_t nranks, int32_t rank, int32_t bc_z, int32_t degree,
+                       int32_t basis, int32_t* out6) {
+  if (!out6 || Nz < 1 || nranks < 1 || rank < 0 || rank >= nranks || Nz < nranks || degree < 1 ||
+      degree > 8)
+    return fail(DG_ERR_PARAM, "bad slab plan arguments");
+  int plan[4];
+  slab_plan(Nz, nranks, rank, bc_z, plan);
+  for (int k = 0; k < 4; ++k) out6[k] = plan[k];
+  out6[4] = (basis == DG_BASIS_HERMITE_LIKE && degree >= 2) ? 2 : degree + 1;
+  out6[5] = 0;
+  return DG_OK;
+}
+
+dg_status dg_halo_pack_host(const double* u_slab, int32_t degree, int32_t basis, int32_t Nx, int32_t Ny,
+                            int32_t nz, double* send_lo, double* send_hi) {
+  if (!u_slab || degree < 1 || degree > 8 || Nx < 1 || Ny < 1 || nz < 1)
+    return fail(DG_ERR_PARAM, "bad halo pack arguments");
+  const int n = degree + 1;
+  const int NL = (basis == DG_BASIS_HERMITE_LIKE && degree >= 2) ? 2 : n;
+  const int64_t pc = (int64_t)Nx * Ny, total = pc * NL * n * n;
+  for (int64_t e = 0; e < total; ++e) {
+    if (send_lo) send_lo[e] = u_slab[halo_src(e, n, NL, pc, nz, false)];
+    if (send_hi) send_hi[e] = u_slab[halo_src(e, n, NL, pc, nz, true)];
+  }
+  return DG_OK;
+}
+
+dg_status dg_mesh_query_halo(dg_mesh m, int64_t* count, int32_t* lo_peer, int32_t* hi_peer) {
+  if (!m) return fail(DG_ERR_PARAM, "NULL mesh");
+  if (count) *count = m->halo_count;
+  if (lo_peer) *lo_peer = m->lo_peer;
+  if (hi_peer) *hi_peer = m->hi_peer;
+  return DG_OK;
+}
+
+dg_status dg_halo_pack(dg_mesh m, const double* u, double* send_lo, double* send_hi, void* stream) {
+  if (!m || !u) return fail(DG_ERR_PARAM, "NULL argument");
+  if (m->halo_count == 0) return DG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  return post_launch(m, launch_halo_pack(u, send_lo, send_hi, m->n, m->NL, (int64_t)m->N[0] * m->N[1],
+                                         m->nz, s), "halo_pack", s);
+}
+
+dg_status dg_halo_set(dg_mesh m, const double* recv_lo, const double* recv_hi, void* stream) {
+  if (!m) return fail(DG_ERR_PARAM, "NULL mesh");
+  if (m->halo_count == 0) return DG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = sizeof(double) * (size_t)m->halo_count;
+  if (recv_lo) CUDA_TRY(cudaMemcpyAsync(m->d_recv_lo, recv_lo, bytes, cudaMemcpyDeviceToDevice, s));
+  if (recv_hi) CUDA_TRY(cudaMemcpyAsync(m->d_recv_hi, recv_hi, bytes, cudaMemcpyDeviceToDevice, s));
+  return DG_OK;
+}
 
 dg_status dg_measure_peak(int32_t kind, double* value, void* stream) {
   if (!value || kind < 0 || kind > 2) return fail(DG_ERR_PARAM, "bad kind or NULL value");
@@ -547,16 +637,9 @@ dg_status dg_apply_laplace(dg_mesh m, const double* u, double* y, int32_t flags,
   if (u == y) return fail(DG_ERR_PARAM, "u and y alias");
   if (flags & ~(DG_APPLY_HALO_READY | DG_APPLY_QUADRATURE)) return fail(DG_ERR_PARAM, "bad flags");
   cudaStream_t s = (cudaStream_t)stream;
-  if (!(flags & DG_APPLY_HALO_READY)) {
-    dg_status st = halo_exchange_impl(m, u, s);
-    if (st != DG_OK) return st;
-  }
   ChebyArgs ch{};
-  GridArgs g = grid_args(m, 0, m->nz);
-  if (m->cartesian && !(flags & DG_APPLY_QUADRATURE))
-    return post_launch(m, launch_kron(m->n, m->NL, KMODE_APPLY, m->kp, g, u, y, ch, s), "kron_apply", s);
-  return post_launch(m, launch_quad(m->n, m->NL, m->geom, KMODE_APPLY, m->qp, m->ga, g, u, y, ch, s),
-                     "quad_apply", s);
+  const bool kron = m->cartesian && !(flags & DG_APPLY_QUADRATURE);
+  return run_pass(m, KMODE_APPLY, kron, u, y, ch, (flags & DG_APPLY_HALO_READY) != 0, s);
 }
 
 dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, void* stream) {
@@ -648,14 +731,7 @@ dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* wor
       rho = rho_n;
     }
     const double* uj = buf[where[j]];
-    st = halo_exchange_impl(m, uj, s);
-    if (st != DG_OK) return st;
-    GridArgs g = grid_args(m, 0, m->nz);
-    if (m->cartesian)
-      st = post_launch(m, launch_kron(m->n, m->NL, mode, m->kp, g, uj, nullptr, ch, s), "kron_cheby", s);
-    else
-      st = post_launch(m, launch_quad(m->n, m->NL, m->geom, mode, m->qp, m->ga, g, uj, nullptr, ch, s),
-                       "quad_cheby", s);
+    st = run_pass(m, mode, m->cartesian, uj, nullptr, ch, false, s);
     if (st != DG_OK) return st;
   }
   if (where[degree] != 0)
@@ -669,8 +745,60 @@ dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* wor
 namespace {
 
 dg_status halo_exchange_impl(dg_mesh m, const double* u, cudaStream_t s) {
-  if (!m->comm) return DG_OK;   // single rank: periodic wrap is read in place
-  return fail(DG_ERR_UNSUPPORTED, "multi-rank halo not in this build");
+  if (m->zlo != ZSRC_HALO && m->zhi != ZSRC_HALO) return DG_OK;
+  if (m->external)
+    return fail(DG_ERR_UNSUPPORTED, "external halo transport: call dg_halo_pack/dg_halo_set and "
+                                    "DG_APPLY_HALO_READY");
+  const int64_t plane_cells = (int64_t)m->N[0] * m->N[1];
+  cudaError_t e = launch_halo_pack(u, m->lo_peer >= 0 ? m->d_send_lo : nullptr,
+                                   m->hi_peer >= 0 ? m->d_send_hi : nullptr, m->n, m->NL, plane_cells,
+                                   m->nz, s);
+  if (e != cudaSuccess) return fail(DG_ERR_CUDA, "halo pack: %s", cudaGetErrorString(e));
+  m->launches++;
+  const size_t cnt = (size_t)m->halo_count;
+  NCCL_TRY(ncclGroupStart());
+  // "up": top layers to the upper peer, lower peer's top layers into recv_lo
+  if (m->hi_peer >= 0) NCCL_TRY(ncclSend(m->d_send_hi, cnt, ncclDouble, m->hi_peer, m->comm, s));
+  if (m->lo_peer >= 0) NCCL_TRY(ncclRecv(m->d_recv_lo, cnt, ncclDouble, m->lo_peer, m->comm, s));
+  // "down": bottom layers to the lower peer, upper peer's bottom layers into recv_hi
+  if (m->lo_peer >= 0) NCCL_TRY(ncclSend(m->d_send_lo, cnt, ncclDouble, m->lo_peer, m->comm, s));
+  if (m->hi_peer >= 0) NCCL_TRY(ncclRecv(m->d_recv_hi, cnt, ncclDouble, m->hi_peer, m->comm, s));
+  NCCL_TRY(ncclGroupEnd());
+  if (debug_sync()) CUDA_TRY(cudaStreamSynchronize(s));
+  return DG_OK;
+}
+
+// One operator pass (apply or fused Chebyshev step) over the owned planes.  With an
+// NCCL halo the exchange runs on the comm stream while the interior planes compute;
+// the two boundary planes follow once the halo has arrived.
+dg_status run_pass(dg_mesh m, int mode, bool kron, const double* u, double* y, const ChebyArgs& ch,
+                   bool halo_ready, cudaStream_t s) {
+  auto launch = [&](int zb, int ze) -> dg_status {
+    if (ze <= zb) return DG_OK;
+    GridArgs g = grid_args(m, zb, ze);
+    cudaError_t e = kron ? launch_kron(m->n, m->NL, mode, m->kp, g, u, y, ch, s)
+                         : launch_quad(m->n, m->NL, m->geom, mode, m->qp, m->ga, g, u, y, ch, s);
+    return post_launch(m, e, kron ? "kron" : "quad", s);
+  };
+  const bool need = (m->zlo == ZSRC_HALO || m->zhi == ZSRC_HALO) && !halo_ready;
+  if (!need) return launch(0, m->nz);
+  if (m->external) return halo_exchange_impl(m, u, s);   // reports the error
+  CUDA_TRY(cudaEventRecord(m->ev_ready, s));
+  CUDA_TRY(cudaStreamWaitEvent(m->comm_stream, m->ev_ready, 0));
+  dg_status st = halo_exchange_impl(m, u, m->comm_stream);
+  if (st != DG_OK) return st;
+  CUDA_TRY(cudaEventRecord(m->ev_halo, m->comm_stream));
+  const int zi0 = m->zlo == ZSRC_HALO ? 1 : 0;
+  const int zi1 = m->zhi == ZSRC_HALO ? m->nz - 1 : m->nz;
+  if (zi1 > zi0) {
+    st = launch(zi0, zi1);
+    if (st != DG_OK) return st;
+  }
+  CUDA_TRY(cudaStreamWaitEvent(s, m->ev_halo, 0));
+  if (zi1 <= zi0) return launch(0, m->nz);
+  st = launch(0, zi0);
+  if (st != DG_OK) return st;
+  return launch(zi1, m->nz);
 }
 
 }  // namespace

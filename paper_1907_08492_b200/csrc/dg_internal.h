@@ -110,6 +110,8 @@ cudaError_t launch_cart_diag(int n, const CartDiagParams& p, int Nx, int Ny, int
                              int Nz_global, double* out, cudaStream_t s);
 
 cudaError_t measure_peak(int kind, double* value, cudaStream_t s);
+cudaError_t launch_halo_pack(const double* u, double* send_lo, double* send_hi, int n, int NL,
+                             int64_t plane_cells, int nz, cudaStream_t s);
 
 // general quadrature path (k_quad.cu) and its setup (k_geom.cu)
 cudaError_t launch_quad(int n, int NL, int geom, int mode, const QuadParams& qp, const GeomArgs& ga,
