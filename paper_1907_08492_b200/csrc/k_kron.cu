@@ -113,7 +113,11 @@ k_kron(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g
   double* F = RF + cslot * Lay::SF;
 
   // ---------------------------------------------------------------- P0: loads
+  // own cell: coalesced; y/z-neighbour layers: coalesced along their contiguous runs into
+  // smem rows; x-neighbour layers: from the neighbouring slot's smem when that cell is in
+  // this block (x-consecutive), else from global into registers here.
   double xm[NL], xp[NL];
+  bool xm_smem = false, xp_smem = false;
   if (active) {
     const int cz = (int)(cid / plane);
     const int rem = (int)(cid - (int64_t)cz * plane);
@@ -122,10 +126,13 @@ k_kron(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g
     double v[N];
 #pragma unroll
     for (int r = 0; r < N; ++r) v[r] = __ldg(own + line + r * NN);
+    xm_smem = cslot > 0 && cx > 0;
+    xp_smem = cslot + 1 < ncell && cx + 1 < g.Nx;
     {
       const int a = line % N, b = line / N;   // this thread's x-line (j, k)
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
+        if (s == 0 ? xm_smem : xp_smem) continue;
         const FaceSrc src = face_source<N, NL>(g, u, cid, cx, cy, cz, s);
 #pragma unroll
         for (int l = 0; l < NL; ++l) {
@@ -136,25 +143,41 @@ k_kron(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g
         }
       }
     }
-    // rows of the y- and z-neighbour layers, swept with M along x
-    for (int job = line; job < 4 * NL * N; job += NN) {
-      const int fr = job / (NL * N), l = (job / N) % NL, b = job % N;
+    // y/z faces: element q of a face in contiguous-address order
+    //   y: (a fastest, then l, then b) -> global (b*N + L)*N + a
+    //   z: (a, b, l)                   -> global (L*N + b)*N + a
+    double fvals[4][NL];
+#pragma unroll
+    for (int fr = 0; fr < 4; ++fr) {
       const int f = 2 + fr, d = f >> 1, s = f & 1;
       const FaceSrc src = face_source<N, NL>(g, u, cid, cx, cy, cz, f);
-      const int L = s == 0 ? N - NL + l : l;
-      const int m = src.reflect ? N - 1 - L : L;
-      double r[N], o[N];
 #pragma unroll
-      for (int i = 0; i < N; ++i) r[i] = src.sign * __ldg(src.base + face_elem<N>(d, m, i, b));
-      eo_apply<N, 1>(kp.M, r, o);
-      double* row = F + fr * Lay::FACE + (l * N + b) * P;
-#pragma unroll
-      for (int i = 0; i < N; ++i) row[i] = o[i];
+      for (int q = 0; q < NL; ++q) {
+        const int e = line + q * NN;
+        int a, l, b;
+        if (d == 1) { a = e % N; l = (e / N) % NL; b = e / (N * NL); }
+        else        { a = e % N; b = (e / N) % N; l = e / NN; }
+        const int L = s == 0 ? N - NL + l : l;
+        const int m = src.reflect ? N - 1 - L : L;
+        fvals[fr][q] = src.sign * __ldg(src.base + face_elem<N>(d, m, a, b));
+      }
     }
 #pragma unroll
     for (int r = 0; r < N; ++r) {
       const int e = line + r * NN;
       U[at(LX, e % N, (e / N) % N, e / NN)] = v[r];
+    }
+#pragma unroll
+    for (int fr = 0; fr < 4; ++fr) {
+      const int d = (2 + fr) >> 1;
+#pragma unroll
+      for (int q = 0; q < NL; ++q) {
+        const int e = line + q * NN;
+        int a, l, b;
+        if (d == 1) { a = e % N; l = (e / N) % NL; b = e / (N * NL); }
+        else        { a = e % N; b = (e / N) % N; l = e / NN; }
+        F[fr * Lay::FACE + (l * N + b) * P + a] = fvals[fr][q];
+      }
     }
   }
   __syncthreads();
@@ -162,6 +185,16 @@ k_kron(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g
   // ---------------------------------------------------------------- x-lines
   if (active) {
     const int j = line % N, k = line / N;
+    if (xm_smem) {
+      const double* Ul = U - LX.CS;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) xm[l] = Ul[at(LX, N - NL + l, j, k)];
+    }
+    if (xp_smem) {
+      const double* Ur = U + LX.CS;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) xp[l] = Ur[at(LX, l, j, k)];
+    }
     double x[N], t[N], a[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) x[i] = U[at(LX, i, j, k)];
@@ -174,6 +207,16 @@ k_kron(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g
     for (int i = 0; i < N; ++i) {
       T[at(LXY, i, j, k)] = t[i];
       A[at(LXY, i, j, k)] = a[i];
+    }
+    // M along x on the rows of the y- and z-neighbour layers (in place)
+    for (int job = line; job < 4 * NL * N; job += NN) {
+      double* row = F + (job / (NL * N)) * Lay::FACE + (job % (NL * N)) * P;
+      double r[N], o[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) r[i] = row[i];
+      eo_apply<N, 1>(kp.M, r, o);
+#pragma unroll
+      for (int i = 0; i < N; ++i) row[i] = o[i];
     }
   }
   __syncthreads();

@@ -40,6 +40,10 @@ struct QLayout {
   static constexpr int PER_CELL = FIELD + 6 * FACE + W + R;
 };
 
+__device__ __forceinline__ double pick3(const double (&v)[3], int i) {
+  return i == 0 ? v[0] : (i == 1 ? v[1] : v[2]);
+}
+
 // own coefficient (d-coordinate m, tangential a, b) in the padded smem field
 template <int N, int P>
 __device__ __forceinline__ int own_idx(int d, int m, int a, int b) {
@@ -76,7 +80,7 @@ __device__ __forceinline__ void face_geom(const QuadParams& qp, const GeomArgs& 
     for (int k = 0; k < 9; ++k) Ji[k] = __ldg(jo + k);
     const double detJ = __ldg(jo + 9);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) r[k] = Ji[d * 3 + k];
+    for (int k = 0; k < 3; ++k) r[k] = d == 0 ? Ji[k] : (d == 1 ? Ji[3 + k] : Ji[6 + k]);
     const double nr = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
     const double ww = qp.w[qa] * qp.w[qb];
     const double fac = nu * ww * detJ;
@@ -98,7 +102,10 @@ __device__ __forceinline__ void face_geom(const QuadParams& qp, const GeomArgs& 
       for (int k = 0; k < 9; ++k) Jn[k] = __ldg(jn + k);
 #pragma unroll
       for (int k = 0; k < 3; ++k) ckp[k] = fac * (Jn[k * 3] * r[0] + Jn[k * 3 + 1] * r[1] + Jn[k * 3 + 2] * r[2]);
-      const double nrp = sqrt(Jn[d * 3] * Jn[d * 3] + Jn[d * 3 + 1] * Jn[d * 3 + 1] + Jn[d * 3 + 2] * Jn[d * 3 + 2]);
+      double rp[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) rp[k] = d == 0 ? Jn[k] : (d == 1 ? Jn[3 + k] : Jn[6 + k]);
+      const double nrp = sqrt(rp[0] * rp[0] + rp[1] * rp[1] + rp[2] * rp[2]);
       sig = ga.pen * 0.5 * (nr + nrp);
     }
     sdA = sig * detJ * nr * ww;
@@ -233,21 +240,22 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
       for (int qb = 0; qb < N; ++qb) {
         double ckm[3], ckp[3], sdA;
         face_geom<N, GEOM>(qp, ga, g, cid, cx, cy, czl, f, qa, qb, ckm, ckp, sdA, mir);
-        const double dotm = ckm[d] * gnm[qb] + ckm[t1] * gam[qb] + ckm[t2] * gbm[qb];
+        const double cmn = pick3(ckm, d), cma = pick3(ckm, t1), cmb = pick3(ckm, t2);
+        const double dotm = cmn * gnm[qb] + cma * gam[qb] + cmb * gbm[qb];
         double jump, avg;
         if (mir) {
           jump = 2.0 * um[qb];
           avg = dotm;
         } else {
-          const double dotp = ckp[d] * gnp[qb] + ckp[t1] * gap[qb] + ckp[t2] * gbp[qb];
+          const double dotp = pick3(ckp, d) * gnp[qb] + pick3(ckp, t1) * gap[qb] + pick3(ckp, t2) * gbp[qb];
           jump = um[qb] - up[qb];
           avg = 0.5 * (dotm + dotp);
         }
         rv[qb] = sdA * jump - avg;
         const double hj = -0.5 * jump;
-        rn[qb] = hj * ckm[d];
-        ra[qb] = hj * ckm[t1];
-        rb[qb] = hj * ckm[t2];
+        rn[qb] = hj * cmn;
+        ra[qb] = hj * cma;
+        rb[qb] = hj * cmb;
       }
       double T1[N], T2[N], T3[N];
       eo_apply<N, 1>(qp.St, rv, T1);
