@@ -33,8 +33,8 @@ struct QLayout {
   static constexpr int P = N | 1;
   static constexpr int FIELD = N * N * P;
   static constexpr int FACE = NL * N * P;
-  static constexpr int FW = 3 * 6 * N * P;          // face work of one round (3 faces x 6 fields)
-  static constexpr int CELLW = 3 * FIELD;           // three work fields of the cell phases
+  static constexpr int FW = 6 * 6 * N * P;
+  static constexpr int CELLW = 5 * FIELD;
   static constexpr int W = FW > CELLW ? FW : CELLW;
   static constexpr int R = 6 * 2 * N * P;
   static constexpr int PER_CELL = FIELD + 6 * FACE + W + R;
@@ -113,21 +113,11 @@ __device__ __forceinline__ void face_geom(const QuadParams& qp, const GeomArgs& 
   }
 }
 
-template <int N, int NL>
-constexpr int qcells_per_block();
-
-template <int N, int NL, int CPB>
-constexpr int quad_min_blocks() {
-  // three resident blocks per SM: caps registers near 150 for ~144-thread blocks
-  return 3;
-}
-
 template <int N, int NL, int CPB, int GEOM, int MODE>
 __global__ void __launch_bounds__(CPB * N * N)
-k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs ga_,
+k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs ga,
        const __grid_constant__ GridArgs g, const double* __restrict__ u, double* __restrict__ y,
        const __grid_constant__ ChebyArgs ch) {
-  const GeomArgs& ga = ga_;
   using Lay = QLayout<N, NL>;
   constexpr int P = Lay::P;
   constexpr int NN = N * N;
@@ -151,233 +141,168 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
   const int crem = (int)(cid - (int64_t)czl * plane);
   const int cy = crem / g.Nx, cx = crem - cy * g.Nx;
 
-  // ---------------------------------------------------------------- P0: staging
-  // own cell coalesced; y/z-neighbour layers coalesced along their contiguous runs;
-  // x-neighbour layers only for cells whose x-neighbour is not the adjacent slot.
+  // ---------------------------------------------------------------- P0
   int mirror_bits = 0;
-  const bool xm_slot = cslot > 0 && cx > 0;
-  const bool xp_slot = cslot + 1 < ncell && cx + 1 < g.Nx;
+  if (active) mirror_bits = stage_cell<N, NL, P, Lay::FACE>(g, u, cid, line, U, FN);
+  __syncthreads();
+
+  // ---------------------------------------------------------------- F1: a-lines
   if (active) {
-    const double* own = u + cid * (int64_t)(N * NN);
-    double v[N];
+    for (int job = line; job < 6 * N; job += NN) {
+      const int f = job / N, b = job % N, d = f >> 1, s = f & 1;
+      double Vm[N], Dm[N], Vp[N], Dp[N];
 #pragma unroll
-    for (int r = 0; r < N; ++r) v[r] = __ldg(own + line + r * NN);
-    double fv[6][NL];
+      for (int a = 0; a < N; ++a) {
+        double v = 0.0, dd = 0.0, vp = 0.0, dp = 0.0;
 #pragma unroll
-    for (int f = 0; f < 6; ++f) {
-      const int d = f >> 1, s = f & 1;
-      const FaceSrc src = face_source<N, NL>(g, u, cid, cx, cy, czl, f);
-      mirror_bits |= src.mirror << f;
-      if (d == 0 && (s == 0 ? xm_slot : xp_slot)) continue;
-#pragma unroll
-      for (int q = 0; q < NL; ++q) {
-        const int e = line + q * NN;
-        int a, l, b;
-        if (d == 0) { a = e % N; b = (e / N) % N; l = e / NN; }
-        else if (d == 1) { a = e % N; l = (e / N) % NL; b = e / (N * NL); }
-        else { a = e % N; b = (e / N) % N; l = e / NN; }
-        const int L = s == 0 ? N - NL + l : l;
-        const int m = src.reflect ? N - 1 - L : L;
-        fv[f][q] = src.sign * __ldg(src.base + face_elem<N>(d, m, a, b));
+        for (int l = 0; l < NL; ++l) {
+          const int L = s ? N - NL + l : l;
+          const double x = U[own_idx<N, P>(d, L, a, b)];
+          v = fma(qp.sf[s][l], x, v);
+          dd = fma(qp.df[s][l], x, dd);
+          const double xn = FN[f * Lay::FACE + (l * N + b) * P + a];
+          vp = fma(qp.sfn[s][l], xn, vp);
+          dp = fma(qp.dfn[s][l], xn, dp);
+        }
+        Vm[a] = v;
+        Dm[a] = dd;
+        Vp[a] = vp;
+        Dp[a] = dp;
       }
-    }
+      double o[N];
+      double* base = W + (f * 6 * N + b) * P;   // field q at base + q*N*P
+      {
+        const EOSplit<N> sv = eo_split<N>(Vm);
+        eo_mul<N, 1, false>(qp.S, sv, o);
 #pragma unroll
-    for (int r = 0; r < N; ++r) {
-      const int e = line + r * NN;
-      U[(e / N) * P + e % N] = v[r];
-    }
+        for (int a = 0; a < N; ++a) base[0 * N * P + a] = o[a];
+        eo_mul<N, -1, false>(qp.D, sv, o);
 #pragma unroll
-    for (int f = 0; f < 6; ++f) {
-      const int d = f >> 1, s = f & 1;
-      if (d == 0 && (s == 0 ? xm_slot : xp_slot)) continue;
+        for (int a = 0; a < N; ++a) base[1 * N * P + a] = o[a];
+        eo_apply<N, 1>(qp.S, Dm, o);
 #pragma unroll
-      for (int q = 0; q < NL; ++q) {
-        const int e = line + q * NN;
-        int a, l, b;
-        if (d == 1) { a = e % N; l = (e / N) % NL; b = e / (N * NL); }
-        else { a = e % N; b = (e / N) % N; l = e / NN; }
-        FN[f * Lay::FACE + (l * N + b) * P + a] = fv[f][q];
+        for (int a = 0; a < N; ++a) base[2 * N * P + a] = o[a];
+      }
+      if (!((mirror_bits >> f) & 1)) {
+        const EOSplit<N> sv = eo_split<N>(Vp);
+        eo_mul<N, 1, false>(qp.S, sv, o);
+#pragma unroll
+        for (int a = 0; a < N; ++a) base[3 * N * P + a] = o[a];
+        eo_mul<N, -1, false>(qp.D, sv, o);
+#pragma unroll
+        for (int a = 0; a < N; ++a) base[4 * N * P + a] = o[a];
+        eo_apply<N, 1>(qp.S, Dp, o);
+#pragma unroll
+        for (int a = 0; a < N; ++a) base[5 * N * P + a] = o[a];
       }
     }
   }
   __syncthreads();
 
-  // ---------------------------------------------------------------- faces, two rounds
-#pragma unroll 1
-  for (int round = 0; round < 2; ++round) {
-    // F1: a-lines of the 3 faces with side s = round
-    if (active) {
-      for (int job = line; job < 3 * N; job += NN) {
-        const int fi = job / N, b = job % N;
-        const int f = 2 * fi + round, d = fi, s = round;
-        double Vm[N], Dm[N], Vp[N], Dp[N];
-        const bool nb_slot = d == 0 && (s == 0 ? xm_slot : xp_slot);
-        const double* NU = U + (s == 0 ? -Lay::PER_CELL : Lay::PER_CELL);
+  // ---------------------------------------------------------------- F2: b-lines + flux
+  if (active) {
+    for (int job = line; job < 6 * N; job += NN) {
+      const int f = job / N, qa = job % N, d = f >> 1;
+      const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
+      const bool mir = (mirror_bits >> f) & 1;
+      double* col = W + (f * 6 * N) * P + qa;     // field q, row b at col[(q*N + b)*P]
+      double x0[N], x1[N], x2[N];
 #pragma unroll
-        for (int a = 0; a < N; ++a) {
-          double vv = 0.0, dd = 0.0, vp = 0.0, dp = 0.0;
-#pragma unroll
-          for (int l = 0; l < NL; ++l) {
-            const int L = s ? N - NL + l : l;
-            const double x = U[own_idx<N, P>(d, L, a, b)];
-            vv = fma(qp.sf[s][l], x, vv);
-            dd = fma(qp.df[s][l], x, dd);
-            const int Ln = s ? l : N - NL + l;
-            const double xn = nb_slot ? NU[own_idx<N, P>(0, Ln, a, b)]
-                                      : FN[f * Lay::FACE + (l * N + b) * P + a];
-            vp = fma(qp.sfn[s][l], xn, vp);
-            dp = fma(qp.dfn[s][l], xn, dp);
-          }
-          Vm[a] = vv;
-          Dm[a] = dd;
-          Vp[a] = vp;
-          Dp[a] = dp;
-        }
-        double o[N];
-        double* base = W + (fi * 6 * N + b) * P;   // field q at base + q*N*P
-        {
-          const EOSplit<N> sv = eo_split<N>(Vm);
-          eo_mul<N, 1, false>(qp.S, sv, o);
-#pragma unroll
-          for (int a = 0; a < N; ++a) base[0 * N * P + a] = o[a];
-          eo_mul<N, -1, false>(qp.D, sv, o);
-#pragma unroll
-          for (int a = 0; a < N; ++a) base[1 * N * P + a] = o[a];
-          eo_apply<N, 1>(qp.S, Dm, o);
-#pragma unroll
-          for (int a = 0; a < N; ++a) base[2 * N * P + a] = o[a];
-        }
-        if (!((mirror_bits >> f) & 1)) {
-          const EOSplit<N> sv = eo_split<N>(Vp);
-          eo_mul<N, 1, false>(qp.S, sv, o);
-#pragma unroll
-          for (int a = 0; a < N; ++a) base[3 * N * P + a] = o[a];
-          eo_mul<N, -1, false>(qp.D, sv, o);
-#pragma unroll
-          for (int a = 0; a < N; ++a) base[4 * N * P + a] = o[a];
-          eo_apply<N, 1>(qp.S, Dp, o);
-#pragma unroll
-          for (int a = 0; a < N; ++a) base[5 * N * P + a] = o[a];
-        }
+      for (int b = 0; b < N; ++b) {
+        x0[b] = col[(0 * N + b) * P];
+        x1[b] = col[(1 * N + b) * P];
+        x2[b] = col[(2 * N + b) * P];
       }
-    }
-    __syncthreads();
-    // F2: b-lines, flux, transposed b-sweeps
-    if (active) {
-      for (int job = line; job < 3 * N; job += NN) {
-        const int fi = job / N, qa = job % N;
-        const int f = 2 * fi + round, d = fi;
-        const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
-        const bool mir = (mirror_bits >> f) & 1;
-        double* col = W + (fi * 6 * N) * P + qa;     // field q, row b at col[(q*N + b)*P]
-        // own side: u-, and dA (J^-1 n_K) . grad_xi u- at the n face points of this column
-        double um[N], dotm[N];
-        {
-          double x0[N], x1[N], x2[N], gb[N], ga[N], gn[N];
-#pragma unroll
-          for (int b = 0; b < N; ++b) {
-            x0[b] = col[(0 * N + b) * P];
-            x1[b] = col[(1 * N + b) * P];
-            x2[b] = col[(2 * N + b) * P];
-          }
-          const EOSplit<N> s0 = eo_split<N>(x0);
-          eo_mul<N, 1, false>(qp.S, s0, um);
-          eo_mul<N, -1, false>(qp.D, s0, gb);
-          eo_apply<N, 1>(qp.S, x1, ga);
-          eo_apply<N, 1>(qp.S, x2, gn);
-#pragma unroll
-          for (int qb = 0; qb < N; ++qb) {
-            double ckm[3], ckp[3], sdA;
-            face_geom<N, GEOM>(qp, ga_, g, cid, cx, cy, czl, f, qa, qb, ckm, ckp, sdA, mir);
-            dotm[qb] = pick3(ckm, d) * gn[qb] + pick3(ckm, t1) * ga[qb] + pick3(ckm, t2) * gb[qb];
-          }
-        }
-        // neighbour side
-        double up[N], dotp[N];
-        if (!mir) {
-          double x0[N], x1[N], x2[N], gb[N], ga[N], gn[N];
-#pragma unroll
-          for (int b = 0; b < N; ++b) {
-            x0[b] = col[(3 * N + b) * P];
-            x1[b] = col[(4 * N + b) * P];
-            x2[b] = col[(5 * N + b) * P];
-          }
-          const EOSplit<N> s0 = eo_split<N>(x0);
-          eo_mul<N, 1, false>(qp.S, s0, up);
-          eo_mul<N, -1, false>(qp.D, s0, gb);
-          eo_apply<N, 1>(qp.S, x1, ga);
-          eo_apply<N, 1>(qp.S, x2, gn);
-#pragma unroll
-          for (int qb = 0; qb < N; ++qb) {
-            double ckm[3], ckp[3], sdA;
-            face_geom<N, GEOM>(qp, ga_, g, cid, cx, cy, czl, f, qa, qb, ckm, ckp, sdA, mir);
-            dotp[qb] = pick3(ckp, d) * gn[qb] + pick3(ckp, t1) * ga[qb] + pick3(ckp, t2) * gb[qb];
-          }
-        }
-        double rv[N], ra[N], rb[N], rn[N];
-#pragma unroll
-        for (int qb = 0; qb < N; ++qb) {
-          double ckm[3], ckp[3], sdA;
-          face_geom<N, GEOM>(qp, ga_, g, cid, cx, cy, czl, f, qa, qb, ckm, ckp, sdA, mir);
-          double jump, avg;
-          if (mir) {
-            jump = 2.0 * um[qb];
-            avg = dotm[qb];
-          } else {
-            jump = um[qb] - up[qb];
-            avg = 0.5 * (dotm[qb] + dotp[qb]);
-          }
-          rv[qb] = sdA * jump - avg;
-          const double hj = -0.5 * jump;
-          rn[qb] = hj * pick3(ckm, d);
-          ra[qb] = hj * pick3(ckm, t1);
-          rb[qb] = hj * pick3(ckm, t2);
-        }
-        double T1[N], T2[N], T3[N];
-        eo_apply<N, 1>(qp.St, rv, T1);
-        eo_apply_add<N, -1>(qp.Dt, rb, T1);
-        eo_apply<N, 1>(qp.St, ra, T2);
-        eo_apply<N, 1>(qp.St, rn, T3);
+      double um[N], gam[N], gbm[N], gnm[N];
+      {
+        const EOSplit<N> s0 = eo_split<N>(x0);
+        eo_mul<N, 1, false>(qp.S, s0, um);
+        eo_mul<N, -1, false>(qp.D, s0, gbm);
+      }
+      eo_apply<N, 1>(qp.S, x1, gam);
+      eo_apply<N, 1>(qp.S, x2, gnm);
+      double up[N], gap[N], gbp[N], gnp[N];
+      if (!mir) {
 #pragma unroll
         for (int b = 0; b < N; ++b) {
-          col[(0 * N + b) * P] = T1[b];
-          col[(1 * N + b) * P] = T2[b];
-          col[(2 * N + b) * P] = T3[b];
+          x0[b] = col[(3 * N + b) * P];
+          x1[b] = col[(4 * N + b) * P];
+          x2[b] = col[(5 * N + b) * P];
         }
+        const EOSplit<N> s0 = eo_split<N>(x0);
+        eo_mul<N, 1, false>(qp.S, s0, up);
+        eo_mul<N, -1, false>(qp.D, s0, gbp);
+        eo_apply<N, 1>(qp.S, x1, gap);
+        eo_apply<N, 1>(qp.S, x2, gnp);
+      }
+      double rv[N], ra[N], rb[N], rn[N];
+#pragma unroll
+      for (int qb = 0; qb < N; ++qb) {
+        double ckm[3], ckp[3], sdA;
+        face_geom<N, GEOM>(qp, ga, g, cid, cx, cy, czl, f, qa, qb, ckm, ckp, sdA, mir);
+        const double cmn = pick3(ckm, d), cma = pick3(ckm, t1), cmb = pick3(ckm, t2);
+        const double dotm = cmn * gnm[qb] + cma * gam[qb] + cmb * gbm[qb];
+        double jump, avg;
+        if (mir) {
+          jump = 2.0 * um[qb];
+          avg = dotm;
+        } else {
+          const double dotp = pick3(ckp, d) * gnp[qb] + pick3(ckp, t1) * gap[qb] + pick3(ckp, t2) * gbp[qb];
+          jump = um[qb] - up[qb];
+          avg = 0.5 * (dotm + dotp);
+        }
+        rv[qb] = sdA * jump - avg;
+        const double hj = -0.5 * jump;
+        rn[qb] = hj * cmn;
+        ra[qb] = hj * cma;
+        rb[qb] = hj * cmb;
+      }
+      double T1[N], T2[N], T3[N];
+      eo_apply<N, 1>(qp.St, rv, T1);
+      eo_apply_add<N, -1>(qp.Dt, rb, T1);
+      eo_apply<N, 1>(qp.St, ra, T2);
+      eo_apply<N, 1>(qp.St, rn, T3);
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        col[(0 * N + b) * P] = T1[b];
+        col[(1 * N + b) * P] = T2[b];
+        col[(2 * N + b) * P] = T3[b];
       }
     }
-    __syncthreads();
-    // F3: a-lines (transposed) -> R
-    if (active) {
-      for (int job = line; job < 3 * N; job += NN) {
-        const int fi = job / N, b = job % N;
-        const int f = 2 * fi + round;
-        const double* base = W + (fi * 6 * N + b) * P;
-        double t1[N], t2[N], t3[N], r0[N], r1[N];
-#pragma unroll
-        for (int a = 0; a < N; ++a) {
-          t1[a] = base[0 * N * P + a];
-          t2[a] = base[1 * N * P + a];
-          t3[a] = base[2 * N * P + a];
-        }
-        eo_apply<N, 1>(qp.St, t1, r0);
-        eo_apply_add<N, -1>(qp.Dt, t2, r0);
-        eo_apply<N, 1>(qp.St, t3, r1);
-        double* rb = R + (f * 2 * N + b) * P;
-#pragma unroll
-        for (int a = 0; a < N; ++a) {
-          rb[a] = r0[a];
-          rb[N * P + a] = r1[a];
-        }
-      }
-    }
-    __syncthreads();
   }
+  __syncthreads();
 
-  double* W0 = W;
-  double* W1 = W + Lay::FIELD;
-  double* W2 = W + 2 * Lay::FIELD;
-  // ---------------------------------------------------------------- X: a = S u, b = DS u
+  // ---------------------------------------------------------------- F3: a-lines (transposed)
+  if (active) {
+    for (int job = line; job < 6 * N; job += NN) {
+      const int f = job / N, b = job % N;
+      const double* base = W + (f * 6 * N + b) * P;
+      double t1[N], t2[N], t3[N], r0[N], r1[N];
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        t1[a] = base[0 * N * P + a];
+        t2[a] = base[1 * N * P + a];
+        t3[a] = base[2 * N * P + a];
+      }
+      eo_apply<N, 1>(qp.St, t1, r0);
+      eo_apply_add<N, -1>(qp.Dt, t2, r0);
+      eo_apply<N, 1>(qp.St, t3, r1);
+      double* rb = R + (f * 2 * N + b) * P;
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        rb[a] = r0[a];
+        rb[N * P + a] = r1[a];
+      }
+    }
+  }
+  __syncthreads();
+
+  double* A = W;
+  double* B = W + Lay::FIELD;
+  double* C1 = W + 2 * Lay::FIELD;
+  double* C2 = W + 3 * Lay::FIELD;
+  double* C3 = W + 4 * Lay::FIELD;
+  // ---------------------------------------------------------------- X
   if (active) {
     const int j = line % N, k = line / N;
     double x[N], o[N];
@@ -386,37 +311,31 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
     const EOSplit<N> sx = eo_split<N>(x);
     eo_mul<N, 1, false>(qp.S, sx, o);
 #pragma unroll
-    for (int i = 0; i < N; ++i) W0[(k * N + j) * P + i] = o[i];
+    for (int i = 0; i < N; ++i) A[(k * N + j) * P + i] = o[i];
     eo_mul<N, -1, false>(qp.D, sx, o);
 #pragma unroll
-    for (int i = 0; i < N; ++i) W1[(k * N + j) * P + i] = o[i];
+    for (int i = 0; i < N; ++i) B[(k * N + j) * P + i] = o[i];
   }
   __syncthreads();
-  // ---------------------------------------------------------------- Y: c1 = S b, c2 = DS a, c3 = S a
-  {
-    double c1[N], c2[N], c3[N];
+  // ---------------------------------------------------------------- Y
+  if (active) {
     const int i = line % N, k = line / N;
-    if (active) {
-      double al[N], bl[N];
+    double al[N], bl[N], o[N];
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        al[j] = W0[(k * N + j) * P + i];
-        bl[j] = W1[(k * N + j) * P + i];
-      }
-      eo_apply<N, 1>(qp.S, bl, c1);
-      const EOSplit<N> sa = eo_split<N>(al);
-      eo_mul<N, -1, false>(qp.D, sa, c2);
-      eo_mul<N, 1, false>(qp.S, sa, c3);
+    for (int j = 0; j < N; ++j) {
+      al[j] = A[(k * N + j) * P + i];
+      bl[j] = B[(k * N + j) * P + i];
     }
-    __syncthreads();
-    if (active) {
+    eo_apply<N, 1>(qp.S, bl, o);
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        W0[(k * N + j) * P + i] = c1[j];
-        W1[(k * N + j) * P + i] = c2[j];
-        W2[(k * N + j) * P + i] = c3[j];
-      }
-    }
+    for (int j = 0; j < N; ++j) C1[(k * N + j) * P + i] = o[j];
+    const EOSplit<N> sa = eo_split<N>(al);
+    eo_mul<N, -1, false>(qp.D, sa, o);
+#pragma unroll
+    for (int j = 0; j < N; ++j) C2[(k * N + j) * P + i] = o[j];
+    eo_mul<N, 1, false>(qp.S, sa, o);
+#pragma unroll
+    for (int j = 0; j < N; ++j) C3[(k * N + j) * P + i] = o[j];
   }
   __syncthreads();
   // ---------------------------------------------------------------- Z (+ q-point work)
@@ -425,9 +344,9 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
     double c1[N], c2[N], c3[N], gx[N], gy[N], gz[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      c1[k] = W0[(k * N + j) * P + i];
-      c2[k] = W1[(k * N + j) * P + i];
-      c3[k] = W2[(k * N + j) * P + i];
+      c1[k] = C1[(k * N + j) * P + i];
+      c2[k] = C2[(k * N + j) * P + i];
+      c3[k] = C3[(k * N + j) * P + i];
     }
     eo_apply<N, 1>(qp.S, c1, gx);
     eo_apply<N, 1>(qp.S, c2, gy);
@@ -439,6 +358,7 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
 #pragma unroll
       for (int q = 0; q < 9; ++q) Ji[q] = __ldg(jo + q);
       const double dj = __ldg(jo + 9);
+      // det J J^-1 J^-T : (a,b) = sum_k Ji[a][k] Ji[b][k]
       Gc[0] = dj * (Ji[0] * Ji[0] + Ji[1] * Ji[1] + Ji[2] * Ji[2]);
       Gc[1] = dj * (Ji[3] * Ji[3] + Ji[4] * Ji[4] + Ji[5] * Ji[5]);
       Gc[2] = dj * (Ji[6] * Ji[6] + Ji[7] * Ji[7] + Ji[8] * Ji[8]);
@@ -474,36 +394,29 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
     eo_apply<N, -1>(qp.Dt, gz, c3);
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      W0[(k * N + j) * P + i] = c1[k];
-      W1[(k * N + j) * P + i] = c2[k];
-      W2[(k * N + j) * P + i] = c3[k];
+      C1[(k * N + j) * P + i] = c1[k];
+      C2[(k * N + j) * P + i] = c2[k];
+      C3[(k * N + j) * P + i] = c3[k];
     }
   }
   __syncthreads();
-  // ---------------------------------------------------------------- YT: e1 = S^T d1, e2 = DS^T d2 + S^T d3
-  {
+  // ---------------------------------------------------------------- YT
+  if (active) {
     const int i = line % N, k = line / N;
-    double e1[N], e2[N];
-    if (active) {
-      double d1[N], d2[N], d3[N];
+    double d1[N], d2[N], d3[N], e[N];
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        d1[j] = W0[(k * N + j) * P + i];
-        d2[j] = W1[(k * N + j) * P + i];
-        d3[j] = W2[(k * N + j) * P + i];
-      }
-      eo_apply<N, 1>(qp.St, d1, e1);
-      eo_apply<N, -1>(qp.Dt, d2, e2);
-      eo_apply_add<N, 1>(qp.St, d3, e2);
+    for (int j = 0; j < N; ++j) {
+      d1[j] = C1[(k * N + j) * P + i];
+      d2[j] = C2[(k * N + j) * P + i];
+      d3[j] = C3[(k * N + j) * P + i];
     }
-    __syncthreads();
-    if (active) {
+    eo_apply<N, 1>(qp.St, d1, e);
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        W0[(k * N + j) * P + i] = e1[j];
-        W1[(k * N + j) * P + i] = e2[j];
-      }
-    }
+    for (int j = 0; j < N; ++j) A[(k * N + j) * P + i] = e[j];
+    eo_apply<N, -1>(qp.Dt, d2, e);
+    eo_apply_add<N, 1>(qp.St, d3, e);
+#pragma unroll
+    for (int j = 0; j < N; ++j) B[(k * N + j) * P + i] = e[j];
   }
   __syncthreads();
   // ---------------------------------------------------------------- XT + face injection
@@ -513,8 +426,8 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
     double e1[N], e2[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      e1[i] = W0[(xk * N + xj) * P + i];
-      e2[i] = W1[(xk * N + xj) * P + i];
+      e1[i] = A[(xk * N + xj) * P + i];
+      e2[i] = B[(xk * N + xj) * P + i];
     }
     eo_apply<N, -1>(qp.Dt, e1, res);
     eo_apply_add<N, 1>(qp.St, e2, res);
@@ -561,10 +474,10 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
   const int64_t xbase = cid * (int64_t)(N * NN) + (xk * N + xj) * N;   // + i
 
   if constexpr (MODE == KMODE_APPLY) {
-    // stage the result for a coalesced store (W2 is free)
+    // stage the result for a coalesced store
     if (active) {
 #pragma unroll
-      for (int i = 0; i < N; ++i) W2[(xk * N + xj) * P + i] = res[i];
+      for (int i = 0; i < N; ++i) C1[(xk * N + xj) * P + i] = res[i];
     }
     __syncthreads();
     if (active) {
@@ -572,12 +485,11 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
 #pragma unroll
       for (int r = 0; r < N; ++r) {
         const int e = line + r * NN;
-        out[e] = W2[(e / N) * P + e % N];
+        out[e] = C1[(e / N) * P + e % N];
       }
     }
     return;
   } else {
-    double* C1 = W2;
     if (active) {
 #pragma unroll
       for (int i = 0; i < N; ++i) res[i] = __ldg(ch.b + xbase + i) - res[i];
@@ -648,6 +560,7 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
     }
   }
 }
+
 
 // Diagonal of the operator for the basis given by `t` (GL for the GL-Jacobi inner
 // preconditioner of Eq. (12), or the working basis for point Jacobi), any geometry:
@@ -749,7 +662,7 @@ cudaError_t launch_diag_n(int geom, const DiagTables& t, const QuadParams& qp, c
 template <int N, int NL>
 constexpr int qcells_per_block() {
   constexpr int byT = (192 + N * N - 1) / (N * N);
-  constexpr int byS = (75 * 1024) / (QLayout<N, NL>::PER_CELL * 8);
+  constexpr int byS = (110 * 1024) / (QLayout<N, NL>::PER_CELL * 8);
   constexpr int c = byT < byS ? byT : byS;
   return c < 1 ? 1 : c;
 }
