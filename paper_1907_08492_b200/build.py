@@ -54,7 +54,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     hdrs = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(ROOT, "include", "dg.h")]
     newest_hdr = max(os.path.getmtime(h) for h in hdrs)
-    objs = []
+    objs, jobs = [], []
     common = ["-O3", "-std=c++17", "-I" + inc, "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s) + ".o")
@@ -67,7 +67,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
         else:
             cmd = ["g++", "-fPIC", "-Wall", "-Wno-unused-function", "-c", s, "-o", o,
                    "-I/usr/local/cuda/include"] + common
-        _run(cmd, verbose)
+        jobs.append(cmd)
+    if jobs:   # independent translation units: compile in parallel
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+            list(ex.map(lambda c: _run(c, verbose), jobs))
     if force or not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
         cmd = ["nvcc", ARCH, "-shared", "-o", OUT] + objs + [
             "-L" + lib, "-lnccl", "-lcudart", "-lquadmath", "-Xlinker", "-rpath=" + lib]

@@ -134,6 +134,15 @@ dg_status post_launch(dg_mesh m, cudaError_t e, const char* what, cudaStream_t s
   return DG_OK;
 }
 
+// Cartesian kernel selection: k_kron4 (z-first) unless DG_KRON=3 asks for k_kron.cu
+bool kron_v4(int n) {
+  static const int v = [] {
+    const char* e = std::getenv("DG_KRON");
+    return e ? std::atoi(e) : 4;
+  }();
+  return v != 3 && kron4_supported(n);
+}
+
 GridArgs grid_args(dg_mesh m, int zbeg, int zend) {
   GridArgs g{};
   g.Nx = m->N[0];
@@ -776,8 +785,13 @@ dg_status run_pass(dg_mesh m, int mode, bool kron, const double* u, double* y, c
   auto launch = [&](int zb, int ze) -> dg_status {
     if (ze <= zb) return DG_OK;
     GridArgs g = grid_args(m, zb, ze);
-    cudaError_t e = kron ? launch_kron(m->n, m->NL, mode, m->kp, g, u, y, ch, s)
-                         : launch_quad(m->n, m->NL, m->geom, mode, m->qp, m->ga, g, u, y, ch, s);
+    cudaError_t e;
+    if (kron && kron_v4(m->n))
+      e = launch_kron4(m->n, m->NL, mode, m->kp, g, u, y, ch, s);
+    else if (kron)
+      e = launch_kron(m->n, m->NL, mode, m->kp, g, u, y, ch, s);
+    else
+      e = launch_quad(m->n, m->NL, m->geom, mode, m->qp, m->ga, g, u, y, ch, s);
     return post_launch(m, e, kron ? "kron" : "quad", s);
   };
   const bool need = (m->zlo == ZSRC_HALO || m->zhi == ZSRC_HALO) && !halo_ready;

@@ -97,6 +97,10 @@ struct MapParams {
 // Launchers (k_kron.cu, k_basis_change.cu, k_setup.cu)
 cudaError_t launch_kron(int n, int NL, int mode, const KronParams& kp, const GridArgs& g,
                         const double* u, double* y, const ChebyArgs& ch, cudaStream_t s);
+// z-first Kronecker kernel (k_kron4.cu), the default Cartesian path for n = 3..9
+bool kron4_supported(int n);
+cudaError_t launch_kron4(int n, int NL, int mode, const KronParams& kp, const GridArgs& g,
+                         const double* u, double* y, const ChebyArgs& ch, cudaStream_t s);
 cudaError_t launch_basis_change(int n, const BchgParams& bp, const double* in, double* out,
                                 int64_t ncells, cudaStream_t s);
 // diagonal of a Cartesian Kronecker operator: d[i,j,k] = sum_d c_d prod(1D diagonals)

@@ -1,0 +1,530 @@
+// Cartesian fast path of the SIPG operator, z-first schedule (k_kron4).
+//
+// Same operator as k_kron.cu: on a Cartesian cell the quadrature operator of Eq. (1)
+// equals the Kronecker form of Eq. (14) (the paper names the
+// reference-coordinate form at PAPER.md:336-344):
+//   y_K = (M (x) M (x) L_z + M (x) L_y (x) M + L_x (x) M (x) M) u_K
+//       + (M_x M_y N_z^{+-}) u_{z+-} + (M_x N_y^{+-} M_z) u_{y+-} + (N_x^{+-} M_y M_z) u_{x+-}
+// (operators act on the index of their direction; N^{+-} touch only the NL = 2 layers
+// of the neighbour next to the face for the Hermite-like basis).
+//
+// Thread mapping: a block is a run of CPB cells of one x-row (grid = x-runs x rows x
+// planes); thread (a, b', cell) = (threadIdx.x, threadIdx.y % NB, threadIdx.y / NB) owns the R lines (a, b' + r*NB),
+// NB = ceil(n/R), of every sweep direction, so per-thread setup and the coefficient
+// loads are amortised over R lines.  Sweeping z first lets the own data and the raw
+// z-neighbour layers stream from HBM along coalesced z-lines:
+//   Z  (line (i,j)):  t = M_z u,  a = L_z u + N_z^{+-} u_{z+-}           -> smem (ZY)
+//      jobs: M_z on the z-lines of the NL y-neighbour layers (-> GY) and of the NL
+//            x-neighbour layers of cells outside the block (-> HT)
+//   Y  (line (i,k)):  b = M_y a + L_y t + N_y^{+-} (M_z u_{y+-}),  c = M_y t  -> smem (YX)
+//      jobs: M_y on HT -> HC
+//   X  (line (j,k)):  y = M_x b + L_x c + N_x^{+-} c_{x+-}
+// where c_{x+-} = (M_y M_z u)_{x+-} at the NL layers next to the face is the c field of
+// the x-neighbour: read from its block slot, from HC (block edges) or, on mirror faces,
+// from the own c reflected and negated.  Mirror faces use the ghost -(own reflected)
+// (PAPER.md:172-174): z from the own line in registers, y from the own t, x from c.
+// The result is staged in smem and written with coalesced stores.
+//
+// Fused Chebyshev step (merged): after X, r = b - Au in x-lines,
+// then P^{-1} r = (T^{-1})^{(x)3} diag(A_GL)^{-1} (T^{-T})^{(x)3} r (Eq. (12), R13)
+// as x: T^{-T}; z: T^{-T}; y: T^{-T}, diag, T^{-1}; x: T^{-1}; z: T^{-1} + the
+// three-term update of Eq. (11) along the z-lines.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "dg_internal.h"
+
+namespace dgb {
+namespace {
+
+struct Lay3 {
+  int Pj, Pk, CS;
+};
+
+// Per n: lines per thread R, cells per block CPB, and the field layouts
+// addr = i + j*Pj + k*Pk + cell*CS chosen by tools/smem_layout_search5.py
+// (ZY: z-write/y-read, YX: y-write/x-read, XZ: x-write/z-read).
+template <int N> struct K4C;
+template <> struct K4C<3> { static constexpr int R = 1, CPB = 32; static constexpr Lay3 ZY{3, 19, 57}, YX{3, 9, 27}, XZ{3, 20, 73}; };
+template <> struct K4C<4> { static constexpr int R = 2, CPB = 30; static constexpr Lay3 ZY{4, 16, 68}, YX{5, 20, 84}, XZ{5, 20, 84}; };
+template <> struct K4C<5> { static constexpr int R = 2, CPB = 16; static constexpr Lay3 ZY{5, 26, 143}, YX{5, 25, 134}, XZ{5, 25, 126}; };
+template <> struct K4C<6> { static constexpr int R = 1, CPB = 8; static constexpr Lay3 ZY{6, 38, 228}, YX{9, 54, 324}, XZ{11, 66, 402}; };
+template <> struct K4C<7> { static constexpr int R = 2, CPB = 10; static constexpr Lay3 ZY{7, 55, 396}, YX{7, 52, 364}, XZ{7, 49, 344}; };
+template <> struct K4C<8> { static constexpr int R = 1, CPB = 4; static constexpr Lay3 ZY{8, 68, 544}, YX{9, 72, 576}, XZ{12, 97, 776}; };
+template <> struct K4C<9> { static constexpr int R = 1, CPB = 3; static constexpr Lay3 ZY{9, 89, 801}, YX{9, 85, 765}, XZ{9, 81, 729}; };
+
+constexpr int imax(int a, int b) { return a > b ? a : b; }
+
+template <int N, int NL>
+struct K4Layout {
+  static constexpr int R = K4C<N>::R, CPB = K4C<N>::CPB;
+  static constexpr int NB = (N + R - 1) / R;          // thread rows per cell
+  static constexpr int TPC = N * NB;                   // threads per cell
+  static constexpr Lay3 ZY = K4C<N>::ZY, YX = K4C<N>::YX, XZ = K4C<N>::XZ;
+  static constexpr int P = N | 1;                      // output staging row pitch
+  static constexpr Lay3 OUT{P, N * P, N * N * P};
+  // R1: T -> B -> (P^-1: z->y, x->z) -> output;  R2: A -> C -> (P^-1: x->z, y->x)
+  static constexpr int S1 = imax(imax(imax(ZY.CS, YX.CS), OUT.CS), XZ.CS);
+  static constexpr int S2 = imax(imax(ZY.CS, YX.CS), XZ.CS);
+  static constexpr int PG = N | 1;
+  static constexpr int GYC = 2 * NL * N * PG;          // y-ghost rows per cell [f][l][k][i]
+  static constexpr int HS = NL * N * PG;               // one x-halo field [l][k][j]
+  static constexpr int doubles() { return CPB * (S1 + S2 + GYC) + 2 * 2 * HS; }
+  static constexpr int bytes() { return doubles() * 8; }
+};
+
+__device__ __forceinline__ int at(const Lay3& L, int i, int j, int k) { return i + j * L.Pj + k * L.Pk; }
+
+template <int N, int NL>
+constexpr int k4_min_blocks() {
+  using L = K4Layout<N, NL>;
+  constexpr int b = (227 * 1024) / L::bytes();
+  constexpr int t = 2048 / (L::CPB * L::TPC);
+  constexpr int m = b < t ? b : t;
+  return m < 1 ? 1 : (m > 3 ? 3 : m);
+}
+
+// M (even-odd) applied to N values read with a stride, written with a stride
+template <int N>
+__device__ __forceinline__ void mass_line(const double* __restrict__ M, const double* src, int ss,
+                                          double* dst, int ds) {
+  double v[N], o[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = src[k * ss];
+  eo_apply<N, 1>(M, v, o);
+#pragma unroll
+  for (int k = 0; k < N; ++k) dst[k * ds] = o[k];
+}
+
+template <int N, int NL, int MODE>
+__global__ void __launch_bounds__(K4Layout<N, NL>::CPB * K4Layout<N, NL>::TPC, (k4_min_blocks<N, NL>()))
+k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g,
+        const double* __restrict__ u, double* __restrict__ y, const __grid_constant__ ChebyArgs ch) {
+  using Lay = K4Layout<N, NL>;
+  constexpr int R = Lay::R, NB = Lay::NB, TPC = Lay::TPC, CPB = Lay::CPB;
+  constexpr int NN = N * N, N3 = N * NN;
+  constexpr Lay3 LZY = Lay::ZY, LYX = Lay::YX, LXZ = Lay::XZ, LOUT = Lay::OUT;
+  constexpr int PG = Lay::PG;
+  extern __shared__ double smem[];
+  double* R1 = smem;
+  double* R2 = R1 + CPB * Lay::S1;
+  double* GYb = R2 + CPB * Lay::S2;
+  double* HX = GYb + CPB * Lay::GYC;   // [h][field: 0 = t, 1 = c][l][k][j]
+
+  const int ta = threadIdx.x, cslot = threadIdx.y / NB, tb = threadIdx.y - cslot * NB;
+  const int lt = ta + N * tb;          // thread index inside the cell
+  const int cx0 = blockIdx.x * CPB;
+  const int cy = blockIdx.y;
+  const int cz = g.zbeg + blockIdx.z;
+  const int ncell = g.Nx - cx0 < CPB ? g.Nx - cx0 : CPB;
+  const bool active = cslot < ncell;
+  const int cx = cx0 + cslot;
+  const int64_t plane = (int64_t)g.Nx * g.Ny;
+  const int64_t rowcell = ((int64_t)cz * g.Ny + cy) * g.Nx;
+  const int64_t cid = rowcell + cx;
+  const double* ucell = u + cid * N3;
+
+  double* GY = GYb + cslot * Lay::GYC;
+
+  // x-neighbour sources of the block edges (halo cell index or -1)
+  const bool xper = g.bc[0] == DG_BC_PERIODIC;
+  int h0 = cx0 > 0 ? cx0 - 1 : (xper ? g.Nx - 1 : -1);
+  int h1 = cx0 + ncell < g.Nx ? cx0 + ncell : (xper ? 0 : -1);
+  if (ncell == g.Nx) h0 = h1 = -1;   // whole row in this block: periodic wrap stays inside
+  const bool need_h0 = cslot == 0 && h0 >= 0;
+  const bool need_h1 = cslot == ncell - 1 && h1 >= 0;
+  // y-neighbour rows (-1: mirror)
+  const bool yper = g.bc[1] == DG_BC_PERIODIC;
+  const int ym_row = cy > 0 ? cy - 1 : (yper ? g.Ny - 1 : -1);
+  const int yp_row = cy + 1 < g.Ny ? cy + 1 : (yper ? 0 : -1);
+
+  // z-neighbour sources for this plane
+  int zsrc[2];
+  const double* zbase[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int nz = cz + (s ? 1 : -1);
+    if (nz >= 0 && nz < g.nz) {
+      zsrc[s] = ZSRC_LOCAL;
+      zbase[s] = ucell + (s ? plane * N3 : -plane * N3);
+    } else {
+      zsrc[s] = s ? g.zhi : g.zlo;
+      zbase[s] = ucell + (s ? -(int64_t)(g.nz - 1) : (int64_t)(g.nz - 1)) * plane * N3;   // periodic wrap
+      if (zsrc[s] == ZSRC_HALO)
+        zbase[s] = (s ? g.halo_hi : g.halo_lo) + ((int64_t)cy * g.Nx + cx) * (NL * NN) -
+                   (s ? 0 : (N - NL) * NN);
+    }
+  }
+
+  // ================================================================ Z
+  if (active) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int zj = tb + r * NB;
+      if (N % R != 0 && zj >= N) break;
+      const int zi = ta;
+      double uz[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) uz[k] = __ldg(ucell + k * NN + zj * N + zi);
+      double zm[NL], zp[NL];
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        const int Lm = N - NL + l, Lp = l;
+        zm[l] = zsrc[0] == ZSRC_MIRROR ? -uz[N - 1 - Lm] : __ldg(zbase[0] + Lm * NN + zj * N + zi);
+        zp[l] = zsrc[1] == ZSRC_MIRROR ? -uz[N - 1 - Lp] : __ldg(zbase[1] + Lp * NN + zj * N + zi);
+      }
+      double t[N], a[N];
+      const EOSplit<N> su = eo_split<N>(uz);
+      eo_mul<N, 1, false>(kp.M, su, t);
+      eo_mul<N, 1, false>(kp.L[2], su, a);
+      dense_add<NL, NL>(kp.Nm[2], zm, &a[0]);
+      dense_add<NL, NL>(kp.Np[2], zp, &a[N - NL]);
+      double* T = R1 + cslot * LZY.CS;
+      double* A = R2 + cslot * LZY.CS;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        T[at(LZY, zi, zj, k)] = t[k];
+        A[at(LZY, zi, zj, k)] = a[k];
+      }
+    }
+  }
+  // Block-level job list (balanced over all threads of the block):
+  //   [0, ncell*NYJ):  y-neighbour z-lines (cell, f, l, i) -> GY = (M_z u_{y+-})[k][j_l][i]
+  //   then NL*N x-halo z-lines (l, j) per needed block edge -> HT[h][l][k][j]
+  {
+    constexpr int NYJ = 2 * NL * N;
+    constexpr int BT = CPB * TPC;
+    const int btid = threadIdx.x + N * threadIdx.y;
+    const int nyj = ncell * NYJ;
+    const int nh0 = h0 >= 0 ? NL * N : 0, nh1 = h1 >= 0 ? NL * N : 0;
+    const int njobs = nyj + nh0 + nh1;
+#pragma unroll 1
+    for (int job = btid; job < njobs; job += BT) {
+      if (job < nyj) {
+        const int c = job / NYJ, jj = job - c * NYJ;
+        const int f = jj / (NL * N), l = (jj / N) % NL, i = jj % N;
+        const int nrow = f ? yp_row : ym_row;
+        if (nrow >= 0) {   // mirror: from the own t in stage Y
+          const int jl = f ? l : N - NL + l;
+          mass_line<N>(kp.M, u + (((int64_t)cz * g.Ny + nrow) * g.Nx + cx0 + c) * N3 + jl * N + i, NN,
+                       GYb + c * Lay::GYC + ((f * NL + l) * N) * PG + i, PG);
+        }
+      } else {
+        const int hj = job - nyj;
+        const int h = hj < nh0 ? 0 : 1;
+        const int q = hj - (h ? nh0 : 0);
+        const int l = q / N, j = q - l * N;
+        const int il = h == 0 ? N - NL + l : l;
+        mass_line<N>(kp.M, u + (rowcell + (h ? h1 : h0)) * N3 + j * N + il, NN,
+                     HX + ((h * 2 + 0) * NL + l) * N * PG + j, PG);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ================================================================ Y
+  {
+    double bl[R][N], cl[R][N];
+    if (active) {
+      const double* T = R1 + cslot * LZY.CS;
+      const double* A = R2 + cslot * LZY.CS;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int yk = tb + r * NB, yi = ta;
+        if (N % R != 0 && yk >= N) break;
+        double al[N], tl[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          al[j] = A[at(LZY, yi, j, yk)];
+          tl[j] = T[at(LZY, yi, j, yk)];
+        }
+        double gym[NL], gyp[NL];
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          gym[l] = ym_row >= 0 ? GY[((0 * NL + l) * N + yk) * PG + yi] : -tl[NL - 1 - l];
+          gyp[l] = yp_row >= 0 ? GY[((1 * NL + l) * N + yk) * PG + yi] : -tl[N - 1 - l];
+        }
+        const EOSplit<N> st = eo_split<N>(tl);
+        eo_mul<N, 1, false>(kp.M, eo_split<N>(al), bl[r]);
+        eo_mul<N, 1, true>(kp.L[1], st, bl[r]);
+        eo_mul<N, 1, false>(kp.M, st, cl[r]);
+        dense_add<NL, NL>(kp.Nm[1], gym, &bl[r][0]);
+        dense_add<NL, NL>(kp.Np[1], gyp, &bl[r][N - NL]);
+      }
+    }
+    {   // halo jobs: HC[h][l][k][j] = M_y HT[h][l][k][:], spread over the block
+      const int btid = threadIdx.x + N * threadIdx.y;
+      const int nh0 = h0 >= 0 ? NL * N : 0, nh1 = h1 >= 0 ? NL * N : 0;
+      for (int job = btid; job < nh0 + nh1; job += CPB * TPC) {
+        const int h = job < nh0 ? 0 : 1;
+        const int q = job - (h ? nh0 : 0);
+        const int l = q / N, k = q - l * N;
+        mass_line<N>(kp.M, HX + (((h * 2 + 0) * NL + l) * N + k) * PG, 1,
+                     HX + (((h * 2 + 1) * NL + l) * N + k) * PG, 1);
+      }
+    }
+    __syncthreads();   // all of T, A read: their regions take B, C
+    if (active) {
+      double* Bf = R1 + cslot * LYX.CS;
+      double* Cf = R2 + cslot * LYX.CS;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int yk = tb + r * NB, yi = ta;
+        if (N % R != 0 && yk >= N) break;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          Bf[at(LYX, yi, j, yk)] = bl[r][j];
+          Cf[at(LYX, yi, j, yk)] = cl[r][j];
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ================================================================ X
+  double res[R][N];
+  if (active) {
+    const double* Bf = R1 + cslot * LYX.CS;
+    const double* Cf = R2 + cslot * LYX.CS;
+    // x-neighbour c source per side: 1 in-block slot offset, 2 halo, 0 mirror
+    const bool inb_m = cslot > 0, inb_p = cslot + 1 < ncell;
+    const bool wrap = xper && ncell == g.Nx;   // periodic row inside the block
+    const int offm = inb_m ? -LYX.CS : (ncell - 1) * LYX.CS;
+    const int offp = inb_p ? LYX.CS : -(ncell - 1) * LYX.CS;
+    const bool slot_m = inb_m || wrap, slot_p = inb_p || wrap;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int xk = tb + r * NB, xj = ta;
+      if (N % R != 0 && xk >= N) break;
+      double bl[N], cl[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        bl[i] = Bf[at(LYX, i, xj, xk)];
+        cl[i] = Cf[at(LYX, i, xj, xk)];
+      }
+      double cxm[NL], cxp[NL];
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        const int Lm = N - NL + l, Lp = l;
+        cxm[l] = slot_m ? Cf[offm + at(LYX, Lm, xj, xk)]
+                        : (need_h0 ? HX[(((0 * 2 + 1) * NL + l) * N + xk) * PG + xj] : -cl[N - 1 - Lm]);
+        cxp[l] = slot_p ? Cf[offp + at(LYX, Lp, xj, xk)]
+                        : (need_h1 ? HX[(((1 * 2 + 1) * NL + l) * N + xk) * PG + xj] : -cl[N - 1 - Lp]);
+      }
+      eo_mul<N, 1, false>(kp.M, eo_split<N>(bl), res[r]);
+      eo_mul<N, 1, true>(kp.L[0], eo_split<N>(cl), res[r]);
+      dense_add<NL, NL>(kp.Nm[0], cxm, &res[r][0]);
+      dense_add<NL, NL>(kp.Np[0], cxp, &res[r][N - NL]);
+    }
+  }
+
+  if constexpr (MODE == KMODE_APPLY) {
+    __syncthreads();   // B, C fully read: R1 takes the output
+    double* O = R1 + cslot * LOUT.CS;
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int xk = tb + r * NB, xj = ta;
+        if (N % R != 0 && xk >= N) break;
+#pragma unroll
+        for (int i = 0; i < N; ++i) O[at(LOUT, i, xj, xk)] = res[r][i];
+      }
+    }
+    __syncthreads();
+    if (active) {
+      // element e = lt + q*TPC of the cell: i = ta, row (j + N k) = tb + q*NB
+      double* out = y + cid * N3;
+#pragma unroll
+      for (int q = 0; q < (NN + NB - 1) / NB; ++q) {
+        const int rowi = tb + q * NB;
+        if (NN % NB == 0 || rowi < NN) out[rowi * N + ta] = O[rowi * LOUT.Pj + ta];
+      }
+    }
+    return;
+  } else {
+    // residual r = b - A u along the x-lines
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int xk = tb + r * NB, xj = ta;
+        if (N % R != 0 && xk >= N) break;
+        const double* bb = ch.b + cid * N3 + (xk * N + xj) * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) res[r][i] = __ldg(bb + i) - res[r][i];
+      }
+    }
+    __syncthreads();   // B, C fully read (C also by the neighbour slots)
+    if constexpr (MODE == KMODE_CHEBY_GL) {
+      double* X2 = R2 + cslot * LXZ.CS;
+      double* Z1 = R1 + cslot * LZY.CS;
+      double* Y2 = R2 + cslot * LYX.CS;
+      double* X1 = R1 + cslot * LXZ.CS;
+      if (active) {   // x: T^{-T}
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int xk = tb + r * NB, xj = ta;
+          if (N % R != 0 && xk >= N) break;
+          double o[N];
+          eo_apply<N, 1>(kp.TiT, res[r], o);
+#pragma unroll
+          for (int i = 0; i < N; ++i) X2[at(LXZ, i, xj, xk)] = o[i];
+        }
+      }
+      __syncthreads();
+      if (active) {   // z: T^{-T}
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int zj = tb + r * NB, zi = ta;
+          if (N % R != 0 && zj >= N) break;
+          double v[N], o[N];
+#pragma unroll
+          for (int k = 0; k < N; ++k) v[k] = X2[at(LXZ, zi, zj, k)];
+          eo_apply<N, 1>(kp.TiT, v, o);
+#pragma unroll
+          for (int k = 0; k < N; ++k) Z1[at(LZY, zi, zj, k)] = o[k];
+        }
+      }
+      __syncthreads();
+      if (active) {   // y: T^{-T}, diag(A_GL)^{-1}, T^{-1}
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int yk = tb + r * NB, yi = ta;
+          if (N % R != 0 && yk >= N) break;
+          double v[N], o[N];
+#pragma unroll
+          for (int j = 0; j < N; ++j) v[j] = Z1[at(LZY, yi, j, yk)];
+          eo_apply<N, 1>(kp.TiT, v, o);
+          const double* dv = ch.dinv + cid * N3 + yk * NN + yi;
+#pragma unroll
+          for (int j = 0; j < N; ++j) o[j] *= __ldg(dv + j * N);
+          eo_apply<N, 1>(kp.Ti, o, v);
+#pragma unroll
+          for (int j = 0; j < N; ++j) Y2[at(LYX, yi, j, yk)] = v[j];
+        }
+      }
+      __syncthreads();
+      if (active) {   // x: T^{-1}
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int xk = tb + r * NB, xj = ta;
+          if (N % R != 0 && xk >= N) break;
+          double v[N], o[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) v[i] = Y2[at(LYX, i, xj, xk)];
+          eo_apply<N, 1>(kp.Ti, v, o);
+#pragma unroll
+          for (int i = 0; i < N; ++i) X1[at(LXZ, i, xj, xk)] = o[i];
+        }
+      }
+      __syncthreads();
+      if (active) {   // z: T^{-1} -> res along the z-lines
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int zj = tb + r * NB, zi = ta;
+          if (N % R != 0 && zj >= N) break;
+          double v[N];
+#pragma unroll
+          for (int k = 0; k < N; ++k) v[k] = X1[at(LXZ, zi, zj, k)];
+          eo_apply<N, 1>(kp.Ti, v, res[r]);
+        }
+      }
+    } else {
+      // point Jacobi: diagonal along the x-lines, then to z-lines through smem
+      double* X1 = R1 + cslot * LXZ.CS;
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int xk = tb + r * NB, xj = ta;
+          if (N % R != 0 && xk >= N) break;
+          const double* dv = ch.dinv + cid * N3 + (xk * N + xj) * N;
+#pragma unroll
+          for (int i = 0; i < N; ++i) X1[at(LXZ, i, xj, xk)] = res[r][i] * __ldg(dv + i);
+        }
+      }
+      __syncthreads();
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int zj = tb + r * NB, zi = ta;
+          if (N % R != 0 && zj >= N) break;
+#pragma unroll
+          for (int k = 0; k < N; ++k) res[r][k] = X1[at(LXZ, zi, zj, k)];
+        }
+      }
+    }
+    // three-term update, Eq. (11), along the z-lines
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int zj = tb + r * NB, zi = ta;
+        if (N % R != 0 && zj >= N) break;
+        const int64_t gbase = cid * N3 + zj * N + zi;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const int64_t gi = gbase + k * NN;
+          const double uj = __ldg(u + gi);   // re-read (L1/L2): saves R*N live registers
+          double v = fma(ch.c_z, res[r][k], uj);
+          if (!ch.first) v = fma(ch.c_prev, uj - ch.u_prev[gi], v);
+          ch.u_next[gi] = v;
+        }
+      }
+    }
+  }
+}
+
+template <int N, int NL, int MODE>
+cudaError_t launch_t(const KronParams& kp, const GridArgs& g, const double* u, double* y,
+                     const ChebyArgs& ch, cudaStream_t s) {
+  using Lay = K4Layout<N, NL>;
+  const int planes = g.zend - g.zbeg;
+  if (planes <= 0 || g.Nx <= 0 || g.Ny <= 0) return cudaSuccess;
+  if (g.Ny > 65535 || planes > 65535) return cudaErrorInvalidValue;
+  const dim3 grid((g.Nx + Lay::CPB - 1) / Lay::CPB, g.Ny, planes);
+  const dim3 block(N, Lay::NB * Lay::CPB);
+  const size_t smem = Lay::bytes();
+  auto kern = k_kron4<N, NL, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, block, smem, s>>>(kp, g, u, y, ch);
+  return cudaGetLastError();
+}
+
+template <int N, int NL>
+cudaError_t launch_mode(int mode, const KronParams& kp, const GridArgs& g, const double* u,
+                        double* y, const ChebyArgs& ch, cudaStream_t s) {
+  switch (mode) {
+    case KMODE_APPLY: return launch_t<N, NL, KMODE_APPLY>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ>(kp, g, u, y, ch, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int N>
+cudaError_t launch_nl(int NL, int mode, const KronParams& kp, const GridArgs& g, const double* u,
+                      double* y, const ChebyArgs& ch, cudaStream_t s) {
+  if (NL == 2 && N > 2) return launch_mode<N, 2>(mode, kp, g, u, y, ch, s);
+  if (NL == N) return launch_mode<N, N>(mode, kp, g, u, y, ch, s);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+// n in 3..9 (p = 2..8); other degrees use k_kron.cu
+bool kron4_supported(int n) { return n >= 3 && n <= 9; }
+
+cudaError_t launch_kron4(int n, int NL, int mode, const KronParams& kp, const GridArgs& g,
+                         const double* u, double* y, const ChebyArgs& ch, cudaStream_t s) {
+  switch (n) {
+    case 3: return launch_nl<3>(NL, mode, kp, g, u, y, ch, s);
+    case 4: return launch_nl<4>(NL, mode, kp, g, u, y, ch, s);
+    case 5: return launch_nl<5>(NL, mode, kp, g, u, y, ch, s);
+    case 6: return launch_nl<6>(NL, mode, kp, g, u, y, ch, s);
+    case 7: return launch_nl<7>(NL, mode, kp, g, u, y, ch, s);
+    case 8: return launch_nl<8>(NL, mode, kp, g, u, y, ch, s);
+    case 9: return launch_nl<9>(NL, mode, kp, g, u, y, ch, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dgb
