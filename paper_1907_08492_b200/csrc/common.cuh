@@ -77,6 +77,42 @@ __device__ __forceinline__ void eo_mul(const double* __restrict__ A, const EOSpl
   }
 }
 
+// y = A1 x1 + A2 x2 (both parity S) with one recombination of the even/odd halves
+template <int N, int S>
+__device__ __forceinline__ void eo_mul2(const double* __restrict__ A1, const EOSplit<N>& s1,
+                                        const double* __restrict__ A2, const EOSplit<N>& s2,
+                                        double (&y)[N]) {
+  constexpr int H = N / 2;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    double ye = 0.0, yo = 0.0;
+    if (N & 1) ye = fma(A2[2 * H * H + i], s2.m, A1[2 * H * H + i] * s1.m);
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      ye = fma(A1[i * H + j], s1.e[j], ye);
+      yo = fma(A1[H * H + i * H + j], s1.o[j], yo);
+    }
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      ye = fma(A2[i * H + j], s2.e[j], ye);
+      yo = fma(A2[H * H + i * H + j], s2.o[j], yo);
+    }
+    y[i] = ye + yo;
+    y[N - 1 - i] = (S > 0) ? (ye - yo) : (yo - ye);
+  }
+  if (N & 1) {
+    const double* R1 = A1 + 2 * H * H + H;
+    const double* R2 = A2 + 2 * H * H + H;
+    double ym = (S > 0) ? fma(R2[H], s2.m, R1[H] * s1.m) : 0.0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      ym = fma(R1[j], (S > 0) ? s1.e[j] : s1.o[j], ym);
+      ym = fma(R2[j], (S > 0) ? s2.e[j] : s2.o[j], ym);
+    }
+    y[H] = ym;
+  }
+}
+
 template <int N, int S>
 __device__ __forceinline__ void eo_apply(const double* __restrict__ A, const double (&x)[N],
                                          double (&y)[N]) {

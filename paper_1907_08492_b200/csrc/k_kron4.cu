@@ -31,6 +31,8 @@
 // three-term update of Eq. (11) along the z-lines.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "dg_internal.h"
 
@@ -84,6 +86,16 @@ constexpr int k4_min_blocks() {
   return m < 1 ? 1 : (m > 3 ? 3 : m);
 }
 
+// L2 prefetch of a contiguous range (all threads of the block cooperate, one
+// prefetch per 128-byte line).  Used to pull in the tile one plane up, which a block
+// scheduled about one wave later will read.
+__device__ __forceinline__ void l2_prefetch(const double* p, int64_t ndoubles, int btid, int bt) {
+  const char* c = reinterpret_cast<const char*>(p);
+  const int64_t bytes = ndoubles * 8;
+  for (int64_t o = (int64_t)btid * 128; o < bytes; o += (int64_t)bt * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(c + o));
+}
+
 // M (even-odd) applied to N values read with a stride, written with a stride
 template <int N>
 __device__ __forceinline__ void mass_line(const double* __restrict__ M, const double* src, int ss,
@@ -96,7 +108,7 @@ __device__ __forceinline__ void mass_line(const double* __restrict__ M, const do
   for (int k = 0; k < N; ++k) dst[k * ds] = o[k];
 }
 
-template <int N, int NL, int MODE>
+template <int N, int NL, int MODE, int OUTD>
 __global__ void __launch_bounds__(K4Layout<N, NL>::CPB * K4Layout<N, NL>::TPC, (k4_min_blocks<N, NL>()))
 k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g,
         const double* __restrict__ u, double* __restrict__ y, const __grid_constant__ ChebyArgs ch) {
@@ -157,6 +169,57 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
   }
 
   // ================================================================ Z
+  // Block-level job list (balanced over all threads of the block):
+  //   [0, ncell*NYJ):  y-neighbour z-lines (cell, f, l, i) -> GY = (M_z u_{y+-})[k][j_l][i]
+  //   then NL*N x-halo z-lines (l, j) per needed block edge -> HT[h][l][k][j]
+  // Every job is "load a z-line (stride n^2), apply M_z, store with stride PG".
+  constexpr int NYJ = 2 * NL * N;
+  constexpr int BT = CPB * TPC;
+  const int btid = threadIdx.x + N * threadIdx.y;
+  const int nyj = ncell * NYJ;
+  const int nh0 = h0 >= 0 ? NL * N : 0, nh1 = h1 >= 0 ? NL * N : 0;
+  const int njobs = nyj + nh0 + nh1;
+  auto job_target = [&](int job, const double*& src, double*& dst) {
+    if (job < nyj) {
+      const int c = job / NYJ, jj = job - c * NYJ;
+      const int f = jj / (NL * N), l = (jj / N) % NL, i = jj % N;
+      const int nrow = f ? yp_row : ym_row;
+      if (nrow < 0) {   // mirror: from the own t in stage Y
+        src = nullptr;
+        return;
+      }
+      const int jl = f ? l : N - NL + l;
+      src = u + (((int64_t)cz * g.Ny + nrow) * g.Nx + cx0 + c) * N3 + jl * N + i;
+      dst = GYb + c * Lay::GYC + ((f * NL + l) * N) * PG + i;
+    } else {
+      const int hj = job - nyj;
+      const int h = hj < nh0 ? 0 : 1;
+      const int q = hj - (h ? nh0 : 0);
+      const int l = q / N, j = q - l * N;
+      const int il = h == 0 ? N - NL + l : l;
+      src = u + (rowcell + (h ? h1 : h0)) * N3 + j * N + il;
+      dst = HX + ((h * 2 + 0) * NL + l) * N * PG + j;
+    }
+  };
+  // next plane's tile (same x-run and row) into L2: its block runs about one wave later
+  if (cz + 1 < g.zend) {
+    const int64_t off = (rowcell + plane + cx0) * N3, cnt = (int64_t)ncell * N3;
+    l2_prefetch(u + off, cnt, btid, BT);
+    if (MODE != KMODE_APPLY) {
+      l2_prefetch(ch.b + off, cnt, btid, BT);
+      l2_prefetch(ch.dinv + off, cnt, btid, BT);
+      if (!ch.first) l2_prefetch(ch.u_prev + off, cnt, btid, BT);
+    }
+  }
+  // the first job's loads are issued together with the own z-lines
+  const double* jsrc = nullptr;
+  double* jdst = nullptr;
+  double jv[N];
+  if (btid < njobs) job_target(btid, jsrc, jdst);
+  if (jsrc) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) jv[k] = __ldg(jsrc + k * NN);
+  }
   if (active) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -188,37 +251,18 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
       }
     }
   }
-  // Block-level job list (balanced over all threads of the block):
-  //   [0, ncell*NYJ):  y-neighbour z-lines (cell, f, l, i) -> GY = (M_z u_{y+-})[k][j_l][i]
-  //   then NL*N x-halo z-lines (l, j) per needed block edge -> HT[h][l][k][j]
-  {
-    constexpr int NYJ = 2 * NL * N;
-    constexpr int BT = CPB * TPC;
-    const int btid = threadIdx.x + N * threadIdx.y;
-    const int nyj = ncell * NYJ;
-    const int nh0 = h0 >= 0 ? NL * N : 0, nh1 = h1 >= 0 ? NL * N : 0;
-    const int njobs = nyj + nh0 + nh1;
+  if (jsrc) {
+    double o[N];
+    eo_apply<N, 1>(kp.M, jv, o);
+#pragma unroll
+    for (int k = 0; k < N; ++k) jdst[k * PG] = o[k];
+  }
 #pragma unroll 1
-    for (int job = btid; job < njobs; job += BT) {
-      if (job < nyj) {
-        const int c = job / NYJ, jj = job - c * NYJ;
-        const int f = jj / (NL * N), l = (jj / N) % NL, i = jj % N;
-        const int nrow = f ? yp_row : ym_row;
-        if (nrow >= 0) {   // mirror: from the own t in stage Y
-          const int jl = f ? l : N - NL + l;
-          mass_line<N>(kp.M, u + (((int64_t)cz * g.Ny + nrow) * g.Nx + cx0 + c) * N3 + jl * N + i, NN,
-                       GYb + c * Lay::GYC + ((f * NL + l) * N) * PG + i, PG);
-        }
-      } else {
-        const int hj = job - nyj;
-        const int h = hj < nh0 ? 0 : 1;
-        const int q = hj - (h ? nh0 : 0);
-        const int l = q / N, j = q - l * N;
-        const int il = h == 0 ? N - NL + l : l;
-        mass_line<N>(kp.M, u + (rowcell + (h ? h1 : h0)) * N3 + j * N + il, NN,
-                     HX + ((h * 2 + 0) * NL + l) * N * PG + j, PG);
-      }
-    }
+  for (int job = btid + BT; job < njobs; job += BT) {
+    const double* src;
+    double* dst;
+    job_target(job, src, dst);
+    if (src) mass_line<N>(kp.M, src, NN, dst, PG);
   }
   __syncthreads();
 
@@ -245,8 +289,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
           gyp[l] = yp_row >= 0 ? GY[((1 * NL + l) * N + yk) * PG + yi] : -tl[N - 1 - l];
         }
         const EOSplit<N> st = eo_split<N>(tl);
-        eo_mul<N, 1, false>(kp.M, eo_split<N>(al), bl[r]);
-        eo_mul<N, 1, true>(kp.L[1], st, bl[r]);
+        eo_mul2<N, 1>(kp.M, eo_split<N>(al), kp.L[1], st, bl[r]);
         eo_mul<N, 1, false>(kp.M, st, cl[r]);
         dense_add<NL, NL>(kp.Nm[1], gym, &bl[r][0]);
         dense_add<NL, NL>(kp.Np[1], gyp, &bl[r][N - NL]);
@@ -311,14 +354,32 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         cxp[l] = slot_p ? Cf[offp + at(LYX, Lp, xj, xk)]
                         : (need_h1 ? HX[(((1 * 2 + 1) * NL + l) * N + xk) * PG + xj] : -cl[N - 1 - Lp]);
       }
-      eo_mul<N, 1, false>(kp.M, eo_split<N>(bl), res[r]);
-      eo_mul<N, 1, true>(kp.L[0], eo_split<N>(cl), res[r]);
+      eo_mul2<N, 1>(kp.M, eo_split<N>(bl), kp.L[0], eo_split<N>(cl), res[r]);
       dense_add<NL, NL>(kp.Nm[0], cxm, &res[r][0]);
       dense_add<NL, NL>(kp.Np[0], cxp, &res[r][N - NL]);
     }
   }
 
-  if constexpr (MODE == KMODE_APPLY) {
+  if constexpr (MODE == KMODE_APPLY && OUTD) {
+    // direct stores along the x-lines (no staging barriers)
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int xk = tb + r * NB, xj = ta;
+        if (N % R != 0 && xk >= N) break;
+        double* out = y + cid * N3 + (xk * N + xj) * N;
+        if constexpr (N % 2 == 0) {
+#pragma unroll
+          for (int i = 0; i < N; i += 2)
+            *reinterpret_cast<double2*>(out + i) = make_double2(res[r][i], res[r][i + 1]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < N; ++i) out[i] = res[r][i];
+        }
+      }
+    }
+    return;
+  } else if constexpr (MODE == KMODE_APPLY) {
     __syncthreads();   // B, C fully read: R1 takes the output
     double* O = R1 + cslot * LOUT.CS;
     if (active) {
@@ -472,7 +533,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
   }
 }
 
-template <int N, int NL, int MODE>
+template <int N, int NL, int MODE, int OUTD>
 cudaError_t launch_t(const KronParams& kp, const GridArgs& g, const double* u, double* y,
                      const ChebyArgs& ch, cudaStream_t s) {
   using Lay = K4Layout<N, NL>;
@@ -482,7 +543,7 @@ cudaError_t launch_t(const KronParams& kp, const GridArgs& g, const double* u, d
   const dim3 grid((g.Nx + Lay::CPB - 1) / Lay::CPB, g.Ny, planes);
   const dim3 block(N, Lay::NB * Lay::CPB);
   const size_t smem = Lay::bytes();
-  auto kern = k_kron4<N, NL, MODE>;
+  auto kern = k_kron4<N, NL, MODE, OUTD>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, block, smem, s>>>(kp, g, u, y, ch);
@@ -492,10 +553,16 @@ cudaError_t launch_t(const KronParams& kp, const GridArgs& g, const double* u, d
 template <int N, int NL>
 cudaError_t launch_mode(int mode, const KronParams& kp, const GridArgs& g, const double* u,
                         double* y, const ChebyArgs& ch, cudaStream_t s) {
+  static const int outd = [] {   // DG_K4_OUT=0: smem-staged coalesced stores (comparison)
+    const char* e = std::getenv("DG_K4_OUT");
+    return e ? std::atoi(e) : (N % 2 == 0 ? 1 : 0);   // measured: direct wins for even n only
+  }();
   switch (mode) {
-    case KMODE_APPLY: return launch_t<N, NL, KMODE_APPLY>(kp, g, u, y, ch, s);
-    case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL>(kp, g, u, y, ch, s);
-    case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ>(kp, g, u, y, ch, s);
+    case KMODE_APPLY:
+      return outd ? launch_t<N, NL, KMODE_APPLY, 1>(kp, g, u, y, ch, s)
+                  : launch_t<N, NL, KMODE_APPLY, 0>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0>(kp, g, u, y, ch, s);
   }
   return cudaErrorInvalidValue;
 }
