@@ -157,6 +157,11 @@ GridArgs grid_args(dg_mesh m, int zbeg, int zend) {
   g.zend = zend;
   g.halo_lo = m->d_recv_lo;
   g.halo_hi = m->d_recv_hi;
+  static const int l2pf = [] {
+    const char* e = std::getenv("DG_L2PF");
+    return e ? std::atoi(e) : 1;
+  }();
+  g.l2pf = l2pf;
   return g;
 }
 

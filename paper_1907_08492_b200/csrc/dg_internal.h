@@ -34,6 +34,7 @@ struct GridArgs {
   int zbeg, zend;             // local planes processed by this launch
   const double* halo_lo;      // [Nx*Ny][NL][n][n]: neighbour layers [n-NL, n) of the plane below
   const double* halo_hi;      // [Nx*Ny][NL][n][n]: neighbour layers [0, NL) of the plane above
+  int l2pf;                   // k_kron4/k_quad: L2 prefetch of the next plane's tile (DG_L2PF, default 1)
 };
 
 enum { KMODE_APPLY = 0, KMODE_CHEBY_GL = 1, KMODE_CHEBY_PJ = 2 };

@@ -202,10 +202,10 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
     }
   };
   // next plane's tile (same x-run and row) into L2: its block runs about one wave later
-  if (cz + 1 < g.zend) {
+  if (g.l2pf && cz + 1 < g.zend) {
     const int64_t off = (rowcell + plane + cx0) * N3, cnt = (int64_t)ncell * N3;
     l2_prefetch(u + off, cnt, btid, BT);
-    if (MODE != KMODE_APPLY) {
+    if (MODE != KMODE_APPLY && g.l2pf > 1) {
       l2_prefetch(ch.b + off, cnt, btid, BT);
       l2_prefetch(ch.dinv + off, cnt, btid, BT);
       if (!ch.first) l2_prefetch(ch.u_prev + off, cnt, btid, BT);
@@ -410,12 +410,116 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         const int xk = tb + r * NB, xj = ta;
         if (N % R != 0 && xk >= N) break;
         const double* bb = ch.b + cid * N3 + (xk * N + xj) * N;
+        if constexpr (N % 2 == 0) {
 #pragma unroll
-        for (int i = 0; i < N; ++i) res[r][i] = __ldg(bb + i) - res[r][i];
+          for (int i = 0; i < N; i += 2) {
+            const double2 bv = __ldg(reinterpret_cast<const double2*>(bb + i));
+            res[r][i] = bv.x - res[r][i];
+            res[r][i + 1] = bv.y - res[r][i + 1];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < N; ++i) res[r][i] = __ldg(bb + i) - res[r][i];
+        }
       }
     }
     __syncthreads();   // B, C fully read (C also by the neighbour slots)
-    if constexpr (MODE == KMODE_CHEBY_GL) {
+    if constexpr (MODE == KMODE_CHEBY_GL && N % 2 == 0) {
+      // even n: x: T^{-T}; y: T^{-T}; z: T^{-T}, diag (coalesced z-lines), T^{-1}; y: T^{-1};
+      // x: T^{-1} + update along the x-lines with 128-bit accesses
+      if (active) {   // x: T^{-T} -> R2 (x-write / y-read)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int xk = tb + r * NB, xj = ta;
+          if (N % R != 0 && xk >= N) break;
+          double o[N];
+          eo_apply<N, 1>(kp.TiT, res[r], o);
+          double* W = R2 + cslot * LYX.CS;
+#pragma unroll
+          for (int i = 0; i < N; ++i) W[at(LYX, i, xj, xk)] = o[i];
+        }
+      }
+      __syncthreads();
+      if (active) {   // y: T^{-T} -> R1 (y-write / z-read)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int yk = tb + r * NB, yi = ta;
+          if (N % R != 0 && yk >= N) break;
+          const double* Rd = R2 + cslot * LYX.CS;
+          double* W = R1 + cslot * LZY.CS;
+          double v[N], o[N];
+#pragma unroll
+          for (int j = 0; j < N; ++j) v[j] = Rd[at(LYX, yi, j, yk)];
+          eo_apply<N, 1>(kp.TiT, v, o);
+#pragma unroll
+          for (int j = 0; j < N; ++j) W[at(LZY, yi, j, yk)] = o[j];
+        }
+      }
+      __syncthreads();
+      if (active) {   // z: T^{-T}, diag(A_GL)^{-1}, T^{-1} -> R2 (z-write / y-read)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int zj = tb + r * NB, zi = ta;
+          if (N % R != 0 && zj >= N) break;
+          const double* Rd = R1 + cslot * LZY.CS;
+          double* W = R2 + cslot * LZY.CS;
+          double v[N], o[N];
+#pragma unroll
+          for (int k = 0; k < N; ++k) v[k] = Rd[at(LZY, zi, zj, k)];
+          eo_apply<N, 1>(kp.TiT, v, o);
+          const double* dv = ch.dinv + cid * N3 + zj * N + zi;
+#pragma unroll
+          for (int k = 0; k < N; ++k) o[k] *= __ldg(dv + k * NN);
+          eo_apply<N, 1>(kp.Ti, o, v);
+#pragma unroll
+          for (int k = 0; k < N; ++k) W[at(LZY, zi, zj, k)] = v[k];
+        }
+      }
+      __syncthreads();
+      if (active) {   // y: T^{-1} -> R1 (y-write / x-read)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int yk = tb + r * NB, yi = ta;
+          if (N % R != 0 && yk >= N) break;
+          const double* Rd = R2 + cslot * LZY.CS;
+          double* W = R1 + cslot * LYX.CS;
+          double v[N], o[N];
+#pragma unroll
+          for (int j = 0; j < N; ++j) v[j] = Rd[at(LZY, yi, j, yk)];
+          eo_apply<N, 1>(kp.Ti, v, o);
+#pragma unroll
+          for (int j = 0; j < N; ++j) W[at(LYX, yi, j, yk)] = o[j];
+        }
+      }
+      __syncthreads();
+      if (active) {   // x: T^{-1}, three-term update (Eq. (11)) along the x-lines
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int xk = tb + r * NB, xj = ta;
+          if (N % R != 0 && xk >= N) break;
+          const double* Rd = R1 + cslot * LYX.CS;
+          double v[N], z[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) v[i] = Rd[at(LYX, i, xj, xk)];
+          eo_apply<N, 1>(kp.Ti, v, z);
+          const int64_t gb = cid * N3 + (xk * N + xj) * N;
+#pragma unroll
+          for (int i = 0; i < N; i += 2) {
+            const double2 uj = __ldg(reinterpret_cast<const double2*>(u + gb + i));
+            double2 o;
+            o.x = fma(ch.c_z, z[i], uj.x);
+            o.y = fma(ch.c_z, z[i + 1], uj.y);
+            if (!ch.first) {
+              const double2 up = *reinterpret_cast<const double2*>(ch.u_prev + gb + i);
+              o.x = fma(ch.c_prev, uj.x - up.x, o.x);
+              o.y = fma(ch.c_prev, uj.y - up.y, o.y);
+            }
+            *reinterpret_cast<double2*>(ch.u_next + gb + i) = o;
+          }
+        }
+      }
+      return;
+    } else if constexpr (MODE == KMODE_CHEBY_GL) {
       double* X2 = R2 + cslot * LXZ.CS;
       double* Z1 = R1 + cslot * LZY.CS;
       double* Y2 = R2 + cslot * LYX.CS;

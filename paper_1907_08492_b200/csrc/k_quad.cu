@@ -113,6 +113,12 @@ __device__ __forceinline__ void face_geom(const QuadParams& qp, const GeomArgs& 
   }
 }
 
+__device__ __forceinline__ void l2_prefetch_range(const double* p, int64_t ndoubles, int tid, int bt) {
+  const char* c = reinterpret_cast<const char*>(p);
+  for (int64_t o = (int64_t)tid * 128; o < ndoubles * 8; o += (int64_t)bt * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(c + o));
+}
+
 template <int N, int NL, int CPB, int GEOM, int MODE>
 __global__ void __launch_bounds__(CPB * N * N)
 k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs ga,
@@ -141,6 +147,16 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
   const int crem = (int)(cid - (int64_t)czl * plane);
   const int cy = crem / g.Nx, cx = crem - cy * g.Nx;
 
+  // L2 prefetch: this block's per-q-point tensors (read in stage Z, after the face
+  // work) and the next plane's tile (u, tensors; its block runs about a wave later)
+  if (GEOM == GEOM_PER_QPOINT && g.l2pf) {
+    const int64_t cnt = (int64_t)ncell * 6 * N * NN;
+    l2_prefetch_range(ga.G + cell0 * (6 * N * NN), cnt, tid, blockDim.x);
+    if (cell0 + plane + ncell <= (int64_t)g.nz * plane) {
+      l2_prefetch_range(ga.G + (cell0 + plane) * (6 * N * NN), cnt, tid, blockDim.x);
+      l2_prefetch_range(u + (cell0 + plane) * (N * NN), (int64_t)ncell * N * NN, tid, blockDim.x);
+    }
+  }
   // ---------------------------------------------------------------- P0
   int mirror_bits = 0;
   if (active) mirror_bits = stage_cell<N, NL, P, Lay::FACE>(g, u, cid, line, U, FN);
