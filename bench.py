@@ -245,6 +245,25 @@ def geometry_bytes_per_dof(spec):
     return 6 * 8 + 3 * 4 * 8 * n * n / n ** 3
 
 
+def measured_traffic(workload, kernel, degrees, alg_bytes_per_step):
+    """DRAM bytes (read + write) per launch of the dominant kernel, from the committed
+    ncu capture profiles/r1_traffic.json (one `ncu --metrics dram__bytes_read.sum,
+    dram__bytes_write.sum` pass of this workload, per degree), averaged over the degrees
+    like `achieved`; None if the capture does not cover this workload/kernel."""
+    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    if not os.path.exists(p):
+        return None, "no committed ncu traffic capture"
+    with open(p) as f:
+        d = json.load(f)
+    ent = d.get(workload, {}).get(kernel)
+    if not ent or any(str(q) not in ent["per_launch_bytes"] for q in degrees):
+        return None, "ncu traffic capture does not cover this configuration"
+    per = [ent["per_launch_bytes"][str(q)] for q in degrees]
+    alg = [ent["algorithmic_bytes"][str(q)] for q in degrees]
+    return float(np.mean(per)), (f"ncu dram read+write per launch, mean over degrees ({ent['source']}); "
+                                 f"measured/algorithmic = {sum(per) / sum(alg):.3f}")
+
+
 WORKLOAD_TEXT = {
     "c4": "C4 degree sweep p=2..8, N_p=round(480/(p+1)) cells per direction, matvec + H->GL basis change "
           "+ degree-5 Chebyshev (GL-Jacobi) per degree",
@@ -377,11 +396,13 @@ def run_ours(a, rank, world, local_rank):
     dom_name = max(dom, key=lambda k: dom[k][1])
     dom = {k: v if v[1] > 0 else [0.0, 1e-30] for k, v in dom.items()}
     ach = dom[dom_name][0] / (dom[dom_name][1] * 1e-3) / 1e9 / world   # per-GPU GB/s
-    kname = "k_kron" if all(sp.geometry == "constant" and sp.deform_amp == 0 for sp in specs) else "k_quad"
-    roofline = {"bound": "hbm", "kernel": {"matvec": f"{kname}<APPLY>", "basis_change": "k_bchg",
-                                           "chebyshev_step": f"{kname}<CHEBY_GL>"}[dom_name],
+    kname = "k_kron4" if all(sp.geometry == "constant" and sp.deform_amp == 0 for sp in specs) else "k_quad"
+    kernel = {"matvec": f"{kname}<APPLY>", "basis_change": "k_bchg",
+              "chebyshev_step": f"{kname}<CHEBY_GL>"}[dom_name]
+    traffic, traffic_note = measured_traffic(a.workload, kernel, degrees, dom[dom_name][0] / max(1, a.steps))
+    roofline = {"bound": "hbm", "kernel": kernel,
                 "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-                "traffic": None, "peak_source": hbm_src,
+                "traffic": traffic, "traffic_note": traffic_note, "peak_source": hbm_src,
                 "note": "achieved = algorithmic bytes (matvec/basis change 16 B/DoF, Chebyshev step "
                         "40 B/DoF, first step 32) / summed CUDA-event time of that op, per GPU"}
     mv_gbs = dom["matvec"][0] / (dom["matvec"][1] * 1e-3) / 1e9 / world

@@ -1,0 +1,49 @@
+"""Build profiles/r1_traffic.json from an ncu CSV of the C4 bench command:
+
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+      --kernel-name-base demangled -k regex:k_kron4 --csv \
+      python bench.py --steps 1 --warmup 0 --quick > traffic.csv
+
+Per degree p (template n = p+1) and mode (0 = APPLY, 1 = CHEBY_GL) the median DRAM
+bytes per launch are recorded next to the algorithmic bytes (16 / 40 B per DoF).
+"""
+import csv
+import json
+import os
+import re
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from synthetic import c4_spec  # noqa: E402
+
+rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10 and r[0] != "ID"]
+hdr = None
+for r in csv.reader(open(sys.argv[1])):
+    if r and r[0] == "ID":
+        hdr = r
+        break
+ki, mi, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+idi = hdr.index("ID")
+per = {}
+for r in rows:
+    m = re.search(r"k_kron4<(?:\(int\))?(\d), (?:\(int\))?(\d), (?:\(int\))?(\d)", r[ki])
+    if not m:
+        continue
+    n, nl, mode = map(int, m.groups())
+    if nl != 2 or mode not in (0, 1):
+        continue
+    key = (n - 1, mode)
+    per.setdefault(key, {}).setdefault(r[idi], {})[r[mi]] = float(r[vi].replace(",", ""))
+out = {"c4": {}}
+for (p, mode), launches in sorted(per.items()):
+    tot = [v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in launches.values()]
+    name = "k_kron4<APPLY>" if mode == 0 else "k_kron4<CHEBY_GL>"
+    ent = out["c4"].setdefault(name, {"per_launch_bytes": {}, "algorithmic_bytes": {}, "launches": {},
+                                      "source": "profiles/r1_traffic_ncu.csv"})
+    nd = c4_spec(p).n_dofs
+    ent["per_launch_bytes"][str(p)] = statistics.median(tot)
+    ent["algorithmic_bytes"][str(p)] = nd * (16.0 if mode == 0 else 40.0)
+    ent["launches"][str(p)] = len(tot)
+json.dump(out, open(sys.argv[2], "w"), indent=1)
+print(json.dumps(out, indent=1))
