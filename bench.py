@@ -420,6 +420,27 @@ def run_ours(a, rank, world, local_rank):
             "roofline": roofline, "matvec_roofline": matvec_roof, "ops": ops,
             "gpu_launches": launches, "clocks": clk.summary()}
 
+    # ---------------------------------------------------------------- FDM smoother (extra)
+    # the same fused Chebyshev sweep around the FDM block-Jacobi
+    # inner preconditioner (Eqs. (13)-(15)); measured after the timed region, not part of
+    # `value`.  Algorithmic bytes 32 B/DoF per step (b, u_j, u_{j-1} in, u_{j+1} out; the
+    # FDM diagonal is computed in the kernel), first step 24.
+    if a.workload in ("c4", "c5") and not a.quick:
+        for s in setups:
+            m_ = s["m"]
+            x2 = torch.zeros_like(s["x"])
+            m_.chebyshev_smooth(s["b"], x2, 1.7, degree=a.cheby_degree, work2=s["work2"], inner="fdm")
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(a.steps):
+                m_.chebyshev_smooth(s["b"], x2, 1.7, degree=a.cheby_degree, work2=s["work2"], inner="fdm")
+            e1.record(stream)
+            barrier()
+            ms = allmax(e0.elapsed_time(e1))
+            nd, cd = s["n_global"], a.cheby_degree
+            ops[s["key"]]["cheby_fdm_step_dofs_per_s"] = nd * cd * a.steps / (ms * 1e-3)
+            ops[s["key"]]["cheby_fdm_sweep_gbs"] = nd * (24.0 + 32.0 * (cd - 1)) * a.steps / (ms * 1e-3) / 1e9
     # ---------------------------------------------------------------- e2e (host buffers)
     if not a.no_e2e and not a.quick:
         h2d = d2h = 0

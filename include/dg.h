@@ -69,7 +69,12 @@ enum {
 /* dg_chebyshev_smooth inner preconditioners */
 enum {
   DG_INNER_GL_JACOBI = 0,    /* P^{-1} = (T^{-1})^{x3} diag(A_GL)^{-1} (T^{-T})^{x3}, Eq. (12) */
-  DG_INNER_POINT_JACOBI = 1  /* P^{-1} = diag(A)^{-1} in the working basis    */
+  DG_INNER_POINT_JACOBI = 1, /* P^{-1} = diag(A)^{-1} in the working basis    */
+  DG_INNER_FDM = 2           /* fast-diagonalisation block Jacobi, Eqs. (13)-(15)
+                                (PAPER.md:2117-2165): P^{-1} = Z^{x3} (Lam (+) Lam (+) Lam)^{-1}
+                                (Z^T)^{x3} with L_DG Z = M Z Lam, Z^T M Z = I of the interior
+                                1D element, used on every cell.  Cartesian meshes only
+                                (DG_ERR_UNSUPPORTED otherwise); no diagonal vector. */
 };
 
 typedef struct dg_mesh_s* dg_mesh;   /* opaque, library-owned, freed by dg_mesh_destroy */

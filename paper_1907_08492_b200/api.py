@@ -17,7 +17,7 @@ BASIS = {"hermite": 0, "gl": 1}
 GEOM = {"constant": 0, "per_cell": 1, "per_qpoint": 2}
 BC = {"dirichlet": 0, "periodic": 1}
 BCHG = {"T": 0, "Tinv": 1, "TT": 2, "TinvT": 3}
-INNER = {"gl_jacobi": 0, "point_jacobi": 1}
+INNER = {"gl_jacobi": 0, "point_jacobi": 1, "fdm": 2}
 APPLY_HALO_READY = 1
 APPLY_QUADRATURE = 2
 

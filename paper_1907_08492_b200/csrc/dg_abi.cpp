@@ -57,6 +57,100 @@ bool debug_sync() {
   } while (0)
 
 // pack an n x n row-major matrix into the even-odd layout of common.cuh
+// FDM setup (Eqs. (13)-(15)): generalized symmetric definite
+// eigenproblem L z = lam M z of the 1D interior element in long double: Cholesky
+// M = C C^T, cyclic Jacobi on K = C^-1 L C^-T, Z = C^-T V (so Z^T M Z = I).  The
+// eigenvectors of this reflection-symmetric pencil are symmetric or antisymmetric;
+// they are packed by parity for the even/odd application in k_kron4.  Returns false
+// if M is not SPD or the parity split fails.
+bool fdm_setup(const double* L, const double* M, int n, KronParams& kp) {
+  typedef long double R;
+  R C[kMaxN][kMaxN] = {}, Ci[kMaxN][kMaxN] = {}, K[kMaxN][kMaxN], V[kMaxN][kMaxN], Z[kMaxN][kMaxN];
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j <= i; ++j) {
+      R acc = M[i * n + j];
+      for (int k = 0; k < j; ++k) acc -= C[i][k] * C[j][k];
+      if (i == j) {
+        if (!(acc > 0)) return false;
+        C[i][i] = std::sqrt(acc);
+      } else {
+        C[i][j] = acc / C[j][j];
+      }
+    }
+  for (int j = 0; j < n; ++j) {   // Ci = C^-1 (lower triangular), column by column
+    for (int i = 0; i < n; ++i) {
+      R acc = (i == j) ? 1 : 0;
+      for (int k = 0; k < i; ++k) acc -= C[i][k] * Ci[k][j];
+      Ci[i][j] = acc / C[i][i];
+    }
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      R acc = 0;
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) acc += Ci[i][a] * L[a * n + b] * Ci[j][b];
+      K[i][j] = acc;
+      V[i][j] = (i == j) ? 1 : 0;
+    }
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    R off = 0;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) off += K[p][q] * K[p][q];
+    if (off < 1e-60L) break;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        if (K[p][q] == 0) continue;
+        const R th = (K[q][q] - K[p][p]) / (2 * K[p][q]);
+        const R t = (th >= 0 ? 1 : -1) / (std::fabs(th) + std::sqrt(th * th + 1));
+        const R c = 1 / std::sqrt(t * t + 1), sn = t * c;
+        for (int k = 0; k < n; ++k) {
+          const R kp_ = K[k][p], kq = K[k][q];
+          K[k][p] = c * kp_ - sn * kq;
+          K[k][q] = sn * kp_ + c * kq;
+        }
+        for (int k = 0; k < n; ++k) {
+          const R kp_ = K[p][k], kq = K[q][k];
+          K[p][k] = c * kp_ - sn * kq;
+          K[q][k] = sn * kp_ + c * kq;
+        }
+        for (int k = 0; k < n; ++k) {
+          const R vp = V[k][p], vq = V[k][q];
+          V[k][p] = c * vp - sn * vq;
+          V[k][q] = sn * vp + c * vq;
+        }
+      }
+  }
+  for (int i = 0; i < n; ++i)      // Z = C^-T V
+    for (int m = 0; m < n; ++m) {
+      R acc = 0;
+      for (int k = 0; k < n; ++k) acc += Ci[k][i] * V[k][m];
+      Z[i][m] = acc;
+    }
+  const int h = n / 2, hs = (n + 1) / 2, ha = n / 2;
+  int ns = 0, na = 0;
+  for (int m = 0; m < n; ++m) {
+    R sym = 0, anti = 0, nrm = 0;
+    for (int i = 0; i < n; ++i) {
+      sym += std::fabs(Z[i][m] - Z[n - 1 - i][m]);
+      anti += std::fabs(Z[i][m] + Z[n - 1 - i][m]);
+      nrm += std::fabs(Z[i][m]);
+    }
+    const bool is_sym = sym < 1e-12L * nrm;
+    const bool is_anti = anti < 1e-12L * nrm;
+    if (is_sym == is_anti) return false;
+    if (is_sym) {
+      if (ns >= hs) return false;
+      for (int i = 0; i < hs; ++i) kp.Zs[i * hs + ns] = (double)Z[i][m];
+      kp.lam[ns++] = (double)K[m][m];
+    } else {
+      if (na >= ha) return false;
+      for (int i = 0; i < h; ++i) kp.Za[i * ha + na] = (double)Z[i][m];
+      kp.lam[hs + na++] = (double)K[m][m];
+    }
+  }
+  return ns == hs && na == ha;
+}
+
 void pack_eo(const double* A, int n, double* out) {
   const int h = n / 2, mid = h;
   int o = 0;
@@ -120,6 +214,7 @@ struct dg_mesh_s {
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   int rank = 0, nranks = 1;
   int64_t launches = 0;
+  bool fdm_ok = false;            // FDM tables built (Cartesian meshes)
 };
 
 namespace {
@@ -402,6 +497,8 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
     transpose(t.Tinv, n, TiT);
     pack_eo(TiT, n, kp.TiT);
     pack_eo(t.Tinv, n, kp.Ti);
+    for (int dd = 0; dd < 3; ++dd) kp.cdir[dd] = V / (m->h[dd] * m->h[dd]);
+    m->fdm_ok = m->cartesian && fdm_setup(t.Lhat, t.Mhat, n, kp);
   }
 
   // z sources and halo
@@ -695,8 +792,10 @@ dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* wor
   const double alpha = lo_frac * lambda_max, beta = hi_frac * lambda_max;
   if (!(alpha > 0 && beta > alpha) || !std::isfinite(beta))
     return fail(DG_ERR_PARAM, "need 0 < lo_frac*lambda_max < hi_frac*lambda_max");
-  if (inner != DG_INNER_GL_JACOBI && inner != DG_INNER_POINT_JACOBI)
+  if (inner != DG_INNER_GL_JACOBI && inner != DG_INNER_POINT_JACOBI && inner != DG_INNER_FDM)
     return fail(DG_ERR_PARAM, "bad inner %d", inner);
+  if (inner == DG_INNER_FDM && !(m->fdm_ok && kron_v4(m->n)))
+    return fail(DG_ERR_UNSUPPORTED, "DG_INNER_FDM needs a Cartesian mesh, degree 2..8 and the k_kron4 path");
   const int64_t nd = m->ndofs_local;
   double* W0 = work2;
   double* W1 = work2 + nd;
@@ -704,11 +803,13 @@ dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* wor
     return fail(DG_ERR_PARAM, "b, x and work2 must not overlap");
   if (degree == 0) return DG_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  const bool fdm = inner == DG_INNER_FDM;
   const bool gl = inner == DG_INNER_GL_JACOBI && m->desc.basis == DG_BASIS_HERMITE_LIKE;
-  double** dsrc = gl ? &m->d_dinv_gl : &m->d_dinv_pj;
-  dg_status st = build_diag(m, inner == DG_INNER_GL_JACOBI, dsrc, s);
+  double* dnone = nullptr;
+  double** dsrc = fdm ? &dnone : (gl ? &m->d_dinv_gl : &m->d_dinv_pj);
+  dg_status st = fdm ? DG_OK : build_diag(m, inner == DG_INNER_GL_JACOBI, dsrc, s);
   if (st != DG_OK) return st;
-  const int mode = gl ? KMODE_CHEBY_GL : KMODE_CHEBY_PJ;
+  const int mode = fdm ? KMODE_CHEBY_FDM : (gl ? KMODE_CHEBY_GL : KMODE_CHEBY_PJ);
 
   // storage of u_j so that u_degree lands in x (in-place updates over u_{j-1})
   double* buf[3] = {x, W0, W1};

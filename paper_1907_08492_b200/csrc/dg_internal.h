@@ -22,6 +22,16 @@ struct KronParams {
   double Np[3][kMaxN * kMaxN]; // [NL][NL]: own rows [n-NL,n) x neighbour layers [0,NL)
   double TiT[kEO];             // T^{-T}, even-odd packed
   double Ti[kEO];              // T^{-1}
+  // FDM block Jacobi (Eqs. (13)-(15)): L_hat Z = M_hat Z diag(lam), Z^T M_hat Z = I, split by
+  // the reflection parity of the eigenvectors (hs symmetric, n - hs antisymmetric ones):
+  //   Zs[i*hs + s] = Z[i][sym s]  for rows i < hs (row n/2 is the middle row for odd n)
+  //   Za[i*ha + a] = Z[i][anti a] for rows i < n/2
+  //   lam[m]: symmetric eigenvalues first, then antisymmetric (the packed eigen index)
+  //   cdir[d] = V / h_d^2 (the direction weights of L_d)
+  double Zs[kMaxN * kMaxN];
+  double Za[kMaxN * kMaxN];
+  double lam[kMaxN];
+  double cdir[3];
 };
 
 // Where the z-neighbour layers of the bottom / top local plane come from.
@@ -37,7 +47,7 @@ struct GridArgs {
   int l2pf;                   // k_kron4/k_quad: L2 prefetch of the next plane's tile (DG_L2PF, default 1)
 };
 
-enum { KMODE_APPLY = 0, KMODE_CHEBY_GL = 1, KMODE_CHEBY_PJ = 2 };
+enum { KMODE_APPLY = 0, KMODE_CHEBY_GL = 1, KMODE_CHEBY_PJ = 2, KMODE_CHEBY_FDM = 3 };
 
 struct ChebyArgs {
   const double* b;

@@ -25,7 +25,7 @@
 // (PAPER.md:172-174): z from the own line in registers, y from the own t, x from c.
 // The result is staged in smem and written with coalesced stores.
 //
-// Fused Chebyshev step (merged): after X, r = b - Au in x-lines,
+// Fused Chebyshev step (merged; inner GL-Jacobi or FDM): after X, r = b - Au,
 // then P^{-1} r = (T^{-1})^{(x)3} diag(A_GL)^{-1} (T^{-T})^{(x)3} r (Eq. (12), R13)
 // as x: T^{-T}; z: T^{-T}; y: T^{-T}, diag, T^{-1}; x: T^{-1}; z: T^{-1} + the
 // three-term update of Eq. (11) along the z-lines.
@@ -44,15 +44,15 @@ struct Lay3 {
 };
 
 // Per n: lines per thread R, cells per block CPB, and the field layouts
-// addr = i + j*Pj + k*Pk + cell*CS chosen by tools/smem_layout_search5.py
+// addr = i + j*Pj + k*Pk + cell*CS chosen by tools/smem_layout_search6.py (half-warp model)
 // (ZY: z-write/y-read, YX: y-write/x-read, XZ: x-write/z-read).
 template <int N> struct K4C;
-template <> struct K4C<3> { static constexpr int R = 1, CPB = 32; static constexpr Lay3 ZY{3, 19, 57}, YX{3, 9, 27}, XZ{3, 20, 73}; };
-template <> struct K4C<4> { static constexpr int R = 2, CPB = 30; static constexpr Lay3 ZY{4, 16, 68}, YX{5, 20, 84}, XZ{5, 20, 84}; };
-template <> struct K4C<5> { static constexpr int R = 2, CPB = 16; static constexpr Lay3 ZY{5, 26, 143}, YX{5, 25, 134}, XZ{5, 25, 126}; };
+template <> struct K4C<3> { static constexpr int R = 1, CPB = 32; static constexpr Lay3 ZY{3, 19, 57}, YX{3, 9, 27}, XZ{3, 18, 57}; };
+template <> struct K4C<4> { static constexpr int R = 2, CPB = 30; static constexpr Lay3 ZY{4, 20, 88}, YX{5, 20, 88}, XZ{5, 20, 84}; };
+template <> struct K4C<5> { static constexpr int R = 2, CPB = 16; static constexpr Lay3 ZY{5, 26, 143}, YX{5, 25, 134}, XZ{5, 25, 139}; };
 template <> struct K4C<6> { static constexpr int R = 1, CPB = 8; static constexpr Lay3 ZY{6, 38, 228}, YX{9, 54, 324}, XZ{11, 66, 402}; };
-template <> struct K4C<7> { static constexpr int R = 2, CPB = 10; static constexpr Lay3 ZY{7, 55, 396}, YX{7, 52, 364}, XZ{7, 49, 344}; };
-template <> struct K4C<8> { static constexpr int R = 1, CPB = 4; static constexpr Lay3 ZY{8, 68, 544}, YX{9, 72, 576}, XZ{12, 97, 776}; };
+template <> struct K4C<7> { static constexpr int R = 2, CPB = 10; static constexpr Lay3 ZY{7, 55, 396}, YX{7, 56, 392}, XZ{7, 49, 344}; };
+template <> struct K4C<8> { static constexpr int R = 1, CPB = 4; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{12, 97, 776}; };
 template <> struct K4C<9> { static constexpr int R = 1, CPB = 3; static constexpr Lay3 ZY{9, 89, 801}, YX{9, 85, 765}, XZ{9, 81, 729}; };
 
 constexpr int imax(int a, int b) { return a > b ? a : b; }
@@ -108,6 +108,80 @@ __device__ __forceinline__ void mass_line(const double* __restrict__ M, const do
   for (int k = 0; k < N; ++k) dst[k * ds] = o[k];
 }
 
+// FDM transforms (Eqs. (13)-(15)), even/odd by eigenvector parity (see KronParams):
+// forward o = Z^T v (output in the packed eigen index), backward y = Z x.
+template <int N>
+__device__ __forceinline__ void fdm_fwd(const KronParams& kp, const double (&v)[N], double (&o)[N]) {
+  constexpr int H = N / 2, HS = (N + 1) / 2, HA = N / 2;
+  double e[H > 0 ? H : 1], od[H > 0 ? H : 1];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    e[i] = v[i] + v[N - 1 - i];
+    od[i] = v[i] - v[N - 1 - i];
+  }
+#pragma unroll
+  for (int s = 0; s < HS; ++s) {
+    double acc = (N & 1) ? kp.Zs[H * HS + s] * v[H] : 0.0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) acc = fma(kp.Zs[i * HS + s], e[i], acc);
+    o[s] = acc;
+  }
+#pragma unroll
+  for (int a = 0; a < HA; ++a) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) acc = fma(kp.Za[i * HA + a], od[i], acc);
+    o[HS + a] = acc;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void fdm_bwd(const KronParams& kp, const double (&x)[N], double (&y)[N]) {
+  constexpr int H = N / 2, HS = (N + 1) / 2, HA = N / 2;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    double E = 0.0, O = 0.0;
+#pragma unroll
+    for (int s = 0; s < HS; ++s) E = fma(kp.Zs[i * HS + s], x[s], E);
+#pragma unroll
+    for (int a = 0; a < HA; ++a) O = fma(kp.Za[i * HA + a], x[HS + a], O);
+    y[i] = E + O;
+    y[N - 1 - i] = E - O;
+  }
+  if (N & 1) {
+    double E = 0.0;
+#pragma unroll
+    for (int s = 0; s < HS; ++s) E = fma(kp.Zs[H * HS + s], x[s], E);
+    y[H] = E;
+  }
+}
+
+// P^{-1} building blocks of the fused Chebyshev step: GL-Jacobi (Eq. (12)) or FDM
+template <int N, int MODE>
+__device__ __forceinline__ void pinv_pre(const KronParams& kp, const double (&v)[N], double (&o)[N]) {
+  if constexpr (MODE == KMODE_CHEBY_FDM) fdm_fwd<N>(kp, v, o);
+  else eo_apply<N, 1>(kp.TiT, v, o);
+}
+template <int N, int MODE>
+__device__ __forceinline__ void pinv_post(const KronParams& kp, const double (&v)[N], double (&o)[N]) {
+  if constexpr (MODE == KMODE_CHEBY_FDM) fdm_bwd<N>(kp, v, o);
+  else eo_apply<N, 1>(kp.Ti, v, o);
+}
+// middle-stage diagonal of P^{-1} on a line with fixed packed indices (a1, a2) in the
+// other two directions (weights c1, c2) and running index m along direction d (weight cd)
+template <int N, int MODE>
+__device__ __forceinline__ void pinv_diag(const KronParams& kp, const double* __restrict__ dinv, int stride,
+                                          double c1, int a1, double c2, int a2, double cd, double (&o)[N]) {
+  if constexpr (MODE == KMODE_CHEBY_FDM) {
+    const double base = fma(c1, kp.lam[a1], c2 * kp.lam[a2]);
+#pragma unroll
+    for (int m = 0; m < N; ++m) o[m] /= fma(cd, kp.lam[m], base);
+  } else {
+#pragma unroll
+    for (int m = 0; m < N; ++m) o[m] *= __ldg(dinv + m * stride);
+  }
+}
+
 template <int N, int NL, int MODE, int OUTD>
 __global__ void __launch_bounds__(K4Layout<N, NL>::CPB * K4Layout<N, NL>::TPC, (k4_min_blocks<N, NL>()))
 k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g,
@@ -124,7 +198,6 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
   double* HX = GYb + CPB * Lay::GYC;   // [h][field: 0 = t, 1 = c][l][k][j]
 
   const int ta = threadIdx.x, cslot = threadIdx.y / NB, tb = threadIdx.y - cslot * NB;
-  const int lt = ta + N * tb;          // thread index inside the cell
   const int cx0 = blockIdx.x * CPB;
   const int cy = blockIdx.y;
   const int cz = g.zbeg + blockIdx.z;
@@ -207,7 +280,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
     l2_prefetch(u + off, cnt, btid, BT);
     if (MODE != KMODE_APPLY && g.l2pf > 1) {
       l2_prefetch(ch.b + off, cnt, btid, BT);
-      l2_prefetch(ch.dinv + off, cnt, btid, BT);
+      if (ch.dinv) l2_prefetch(ch.dinv + off, cnt, btid, BT);
       if (!ch.first) l2_prefetch(ch.u_prev + off, cnt, btid, BT);
     }
   }
@@ -424,7 +497,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
       }
     }
     __syncthreads();   // B, C fully read (C also by the neighbour slots)
-    if constexpr (MODE == KMODE_CHEBY_GL && N % 2 == 0) {
+    if constexpr ((MODE == KMODE_CHEBY_GL || MODE == KMODE_CHEBY_FDM) && N % 2 == 0) {
       // even n: x: T^{-T}; y: T^{-T}; z: T^{-T}, diag (coalesced z-lines), T^{-1}; y: T^{-1};
       // x: T^{-1} + update along the x-lines with 128-bit accesses
       if (active) {   // x: T^{-T} -> R2 (x-write / y-read)
@@ -433,7 +506,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
           const int xk = tb + r * NB, xj = ta;
           if (N % R != 0 && xk >= N) break;
           double o[N];
-          eo_apply<N, 1>(kp.TiT, res[r], o);
+          pinv_pre<N, MODE>(kp, res[r], o);
           double* W = R2 + cslot * LYX.CS;
 #pragma unroll
           for (int i = 0; i < N; ++i) W[at(LYX, i, xj, xk)] = o[i];
@@ -450,7 +523,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
           double v[N], o[N];
 #pragma unroll
           for (int j = 0; j < N; ++j) v[j] = Rd[at(LYX, yi, j, yk)];
-          eo_apply<N, 1>(kp.TiT, v, o);
+          pinv_pre<N, MODE>(kp, v, o);
 #pragma unroll
           for (int j = 0; j < N; ++j) W[at(LZY, yi, j, yk)] = o[j];
         }
@@ -466,11 +539,10 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
           double v[N], o[N];
 #pragma unroll
           for (int k = 0; k < N; ++k) v[k] = Rd[at(LZY, zi, zj, k)];
-          eo_apply<N, 1>(kp.TiT, v, o);
-          const double* dv = ch.dinv + cid * N3 + zj * N + zi;
-#pragma unroll
-          for (int k = 0; k < N; ++k) o[k] *= __ldg(dv + k * NN);
-          eo_apply<N, 1>(kp.Ti, o, v);
+          pinv_pre<N, MODE>(kp, v, o);
+          pinv_diag<N, MODE>(kp, ch.dinv + cid * N3 + zj * N + zi, NN, kp.cdir[0], zi, kp.cdir[1], zj,
+                             kp.cdir[2], o);
+          pinv_post<N, MODE>(kp, o, v);
 #pragma unroll
           for (int k = 0; k < N; ++k) W[at(LZY, zi, zj, k)] = v[k];
         }
@@ -486,7 +558,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
           double v[N], o[N];
 #pragma unroll
           for (int j = 0; j < N; ++j) v[j] = Rd[at(LZY, yi, j, yk)];
-          eo_apply<N, 1>(kp.Ti, v, o);
+          pinv_post<N, MODE>(kp, v, o);
 #pragma unroll
           for (int j = 0; j < N; ++j) W[at(LYX, yi, j, yk)] = o[j];
         }
@@ -501,7 +573,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
           double v[N], z[N];
 #pragma unroll
           for (int i = 0; i < N; ++i) v[i] = Rd[at(LYX, i, xj, xk)];
-          eo_apply<N, 1>(kp.Ti, v, z);
+          pinv_post<N, MODE>(kp, v, z);
           const int64_t gb = cid * N3 + (xk * N + xj) * N;
 #pragma unroll
           for (int i = 0; i < N; i += 2) {
@@ -519,7 +591,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         }
       }
       return;
-    } else if constexpr (MODE == KMODE_CHEBY_GL) {
+    } else if constexpr (MODE == KMODE_CHEBY_GL || MODE == KMODE_CHEBY_FDM) {
       double* X2 = R2 + cslot * LXZ.CS;
       double* Z1 = R1 + cslot * LZY.CS;
       double* Y2 = R2 + cslot * LYX.CS;
@@ -530,7 +602,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
           const int xk = tb + r * NB, xj = ta;
           if (N % R != 0 && xk >= N) break;
           double o[N];
-          eo_apply<N, 1>(kp.TiT, res[r], o);
+          pinv_pre<N, MODE>(kp, res[r], o);
 #pragma unroll
           for (int i = 0; i < N; ++i) X2[at(LXZ, i, xj, xk)] = o[i];
         }
@@ -544,7 +616,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
           double v[N], o[N];
 #pragma unroll
           for (int k = 0; k < N; ++k) v[k] = X2[at(LXZ, zi, zj, k)];
-          eo_apply<N, 1>(kp.TiT, v, o);
+          pinv_pre<N, MODE>(kp, v, o);
 #pragma unroll
           for (int k = 0; k < N; ++k) Z1[at(LZY, zi, zj, k)] = o[k];
         }
@@ -558,11 +630,10 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
           double v[N], o[N];
 #pragma unroll
           for (int j = 0; j < N; ++j) v[j] = Z1[at(LZY, yi, j, yk)];
-          eo_apply<N, 1>(kp.TiT, v, o);
-          const double* dv = ch.dinv + cid * N3 + yk * NN + yi;
-#pragma unroll
-          for (int j = 0; j < N; ++j) o[j] *= __ldg(dv + j * N);
-          eo_apply<N, 1>(kp.Ti, o, v);
+          pinv_pre<N, MODE>(kp, v, o);
+          pinv_diag<N, MODE>(kp, ch.dinv + cid * N3 + yk * NN + yi, N, kp.cdir[0], yi, kp.cdir[2], yk,
+                             kp.cdir[1], o);
+          pinv_post<N, MODE>(kp, o, v);
 #pragma unroll
           for (int j = 0; j < N; ++j) Y2[at(LYX, yi, j, yk)] = v[j];
         }
@@ -576,7 +647,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
           double v[N], o[N];
 #pragma unroll
           for (int i = 0; i < N; ++i) v[i] = Y2[at(LYX, i, xj, xk)];
-          eo_apply<N, 1>(kp.Ti, v, o);
+          pinv_post<N, MODE>(kp, v, o);
 #pragma unroll
           for (int i = 0; i < N; ++i) X1[at(LXZ, i, xj, xk)] = o[i];
         }
@@ -590,7 +661,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
           double v[N];
 #pragma unroll
           for (int k = 0; k < N; ++k) v[k] = X1[at(LXZ, zi, zj, k)];
-          eo_apply<N, 1>(kp.Ti, v, res[r]);
+          pinv_post<N, MODE>(kp, v, res[r]);
         }
       }
     } else {
@@ -667,6 +738,7 @@ cudaError_t launch_mode(int mode, const KronParams& kp, const GridArgs& g, const
                   : launch_t<N, NL, KMODE_APPLY, 0>(kp, g, u, y, ch, s);
     case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0>(kp, g, u, y, ch, s);
     case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0>(kp, g, u, y, ch, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -177,6 +177,42 @@ def test_chebyshev(p, inner, degree):
     assert _rel(x.cpu().numpy(), ref) <= TOL
 
 
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("degree", [1, 3])
+def test_chebyshev_fdm(p, degree):
+    """Chebyshev around the FDM block-Jacobi inner preconditioner (Eqs. (13)-(15),
+    PAPER.md:2117-2165) against oracle/fdm.py on an anisotropic, ragged mesh with
+    mixed boundary conditions (interior-element matrices on every cell)."""
+    _needs_gpu()
+    from oracle import fdm
+    from oracle import smoother as sm
+    from oracle.geometry import mesh_from_spec
+    from oracle.sipg import SIPG
+    spec = MeshSpec(degree=p, n_cells=(3, 2, 4), box_hi=(1.0, 0.8, 1.3),
+                    bc=("dirichlet", "periodic", "dirichlet"), seed=70 + p)
+    om = mesh_from_spec(spec)
+    H = SIPG(om, p)
+    P = fdm.FDM(p, (1.0 / 3, 0.8 / 2, 1.3 / 4))
+    b = uniform_vector(spec.n_dofs, 700 + p)
+    x0 = uniform_vector(spec.n_dofs, 800 + p)
+    lmax = 1.7
+    ref = sm.chebyshev(H.apply, P, b, x0, degree, lmax)
+    m = _gpu_mesh(spec)
+    x = _dev(x0)
+    m.chebyshev_smooth(_dev(b), x, lmax, degree=degree, inner="fdm")
+    assert _rel(x.cpu().numpy(), ref) <= TOL
+
+
+def test_fdm_unsupported_on_curved_mesh():
+    _needs_gpu()
+    spec = MeshSpec(degree=3, n_cells=(2, 2, 2), deform_amp=0.05, geometry="per_qpoint", seed=1)
+    m = _gpu_mesh(spec)
+    b = _dev(uniform_vector(spec.n_dofs, 1))
+    x = torch.zeros_like(b)
+    with pytest.raises(Exception, match="FDM"):
+        m.chebyshev_smooth(b, x, 2.0, degree=1, inner="fdm")
+
+
 def _sample_cells(N, k, rng):
     Nx, Ny, Nz = N
     corners = [0, Nx - 1, Nx * Ny - 1, Nx * Ny * Nz - 1, Nx * Ny * (Nz - 1)]
