@@ -238,6 +238,15 @@ bool kron_v4(int n) {
   return v != 3 && kron4_supported(n);
 }
 
+// general kernel selection: k_quad3 (z-first) unless DG_QUAD=1 asks for k_quad.cu
+bool quad_v3(int n, int geom) {
+  static const int v = [] {
+    const char* e = std::getenv("DG_QUAD");
+    return e ? std::atoi(e) : 3;
+  }();
+  return v != 1 && quad3_supported(n, geom);
+}
+
 GridArgs grid_args(dg_mesh m, int zbeg, int zend) {
   GridArgs g{};
   g.Nx = m->N[0];
@@ -896,6 +905,8 @@ dg_status run_pass(dg_mesh m, int mode, bool kron, const double* u, double* y, c
       e = launch_kron4(m->n, m->NL, mode, m->kp, g, u, y, ch, s);
     else if (kron)
       e = launch_kron(m->n, m->NL, mode, m->kp, g, u, y, ch, s);
+    else if (quad_v3(m->n, m->geom))
+      e = launch_quad3(m->n, m->NL, m->geom, mode, m->qp, m->ga, g, u, y, ch, s);
     else
       e = launch_quad(m->n, m->NL, m->geom, mode, m->qp, m->ga, g, u, y, ch, s);
     return post_launch(m, e, kron ? "kron" : "quad", s);

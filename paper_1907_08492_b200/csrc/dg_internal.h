@@ -132,6 +132,11 @@ cudaError_t launch_halo_pack(const double* u, double* send_lo, double* send_hi, 
 cudaError_t launch_quad(int n, int NL, int geom, int mode, const QuadParams& qp, const GeomArgs& ga,
                         const GridArgs& g, const double* u, double* y, const ChebyArgs& ch,
                         cudaStream_t s);
+// z-first quadrature kernel (k_quad3.cu): constant or per-q-point geometry, n = 3..9
+bool quad3_supported(int n, int geom);
+cudaError_t launch_quad3(int n, int NL, int geom, int mode, const QuadParams& qp, const GeomArgs& ga,
+                         const GridArgs& g, const double* u, double* y, const ChebyArgs& ch,
+                         cudaStream_t s);
 cudaError_t launch_geom_qpoint(int n, const MapParams& mp, int Nx, int Ny, int nz, double* G,
                                double* face[3], int* err_flag, cudaStream_t s);
 // diagonal of the operator in a basis given by tables (S, DS, v0, v1, d0, d1 at the

@@ -46,7 +46,7 @@ struct Lay3 {
 // Per n: lines per thread R, cells per block CPB, and the field layouts
 // addr = i + j*Pj + k*Pk + cell*CS chosen by tools/smem_layout_search6.py (half-warp model)
 // (ZY: z-write/y-read, YX: y-write/x-read, XZ: x-write/z-read).
-template <int N> struct K4C;
+template <int N, int ALT = 0> struct K4C;
 template <> struct K4C<3> { static constexpr int R = 1, CPB = 32; static constexpr Lay3 ZY{3, 19, 57}, YX{3, 9, 27}, XZ{3, 18, 57}; };
 template <> struct K4C<4> { static constexpr int R = 2, CPB = 30; static constexpr Lay3 ZY{4, 20, 88}, YX{5, 20, 88}, XZ{5, 20, 84}; };
 template <> struct K4C<5> { static constexpr int R = 2, CPB = 16; static constexpr Lay3 ZY{5, 26, 143}, YX{5, 25, 134}, XZ{5, 25, 139}; };
@@ -54,15 +54,19 @@ template <> struct K4C<6> { static constexpr int R = 1, CPB = 8; static constexp
 template <> struct K4C<7> { static constexpr int R = 2, CPB = 10; static constexpr Lay3 ZY{7, 55, 396}, YX{7, 56, 392}, XZ{7, 49, 344}; };
 template <> struct K4C<8> { static constexpr int R = 1, CPB = 4; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{12, 97, 776}; };
 template <> struct K4C<9> { static constexpr int R = 1, CPB = 3; static constexpr Lay3 ZY{9, 89, 801}, YX{9, 85, 765}, XZ{9, 81, 729}; };
+// alternates (DG_K4_ALT=1): two lines per thread
+template <> struct K4C<6, 1> { static constexpr int R = 2, CPB = 16; static constexpr Lay3 ZY{6, 38, 242}, YX{9, 54, 338}, XZ{6, 36, 217}; };
+template <> struct K4C<8, 1> { static constexpr int R = 2, CPB = 8; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{9, 72, 576}; };
+template <int N> struct K4HasAlt { static constexpr bool value = N == 6 || N == 8; };
 
 constexpr int imax(int a, int b) { return a > b ? a : b; }
 
-template <int N, int NL>
+template <int N, int NL, int ALT = 0>
 struct K4Layout {
-  static constexpr int R = K4C<N>::R, CPB = K4C<N>::CPB;
+  static constexpr int R = K4C<N, ALT>::R, CPB = K4C<N, ALT>::CPB;
   static constexpr int NB = (N + R - 1) / R;          // thread rows per cell
   static constexpr int TPC = N * NB;                   // threads per cell
-  static constexpr Lay3 ZY = K4C<N>::ZY, YX = K4C<N>::YX, XZ = K4C<N>::XZ;
+  static constexpr Lay3 ZY = K4C<N, ALT>::ZY, YX = K4C<N, ALT>::YX, XZ = K4C<N, ALT>::XZ;
   static constexpr int P = N | 1;                      // output staging row pitch
   static constexpr Lay3 OUT{P, N * P, N * N * P};
   // R1: T -> B -> (P^-1: z->y, x->z) -> output;  R2: A -> C -> (P^-1: x->z, y->x)
@@ -77,9 +81,9 @@ struct K4Layout {
 
 __device__ __forceinline__ int at(const Lay3& L, int i, int j, int k) { return i + j * L.Pj + k * L.Pk; }
 
-template <int N, int NL>
+template <int N, int NL, int ALT>
 constexpr int k4_min_blocks() {
-  using L = K4Layout<N, NL>;
+  using L = K4Layout<N, NL, ALT>;
   constexpr int b = (227 * 1024) / L::bytes();
   constexpr int t = 2048 / (L::CPB * L::TPC);
   constexpr int m = b < t ? b : t;
@@ -182,11 +186,11 @@ __device__ __forceinline__ void pinv_diag(const KronParams& kp, const double* __
   }
 }
 
-template <int N, int NL, int MODE, int OUTD>
-__global__ void __launch_bounds__(K4Layout<N, NL>::CPB * K4Layout<N, NL>::TPC, (k4_min_blocks<N, NL>()))
+template <int N, int NL, int MODE, int OUTD, int ALT>
+__global__ void __launch_bounds__(K4Layout<N, NL, ALT>::CPB * K4Layout<N, NL, ALT>::TPC, (k4_min_blocks<N, NL, ALT>()))
 k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g,
         const double* __restrict__ u, double* __restrict__ y, const __grid_constant__ ChebyArgs ch) {
-  using Lay = K4Layout<N, NL>;
+  using Lay = K4Layout<N, NL, ALT>;
   constexpr int R = Lay::R, NB = Lay::NB, TPC = Lay::TPC, CPB = Lay::CPB;
   constexpr int NN = N * N, N3 = N * NN;
   constexpr Lay3 LZY = Lay::ZY, LYX = Lay::YX, LXZ = Lay::XZ, LOUT = Lay::OUT;
@@ -708,17 +712,17 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
   }
 }
 
-template <int N, int NL, int MODE, int OUTD>
+template <int N, int NL, int MODE, int OUTD, int ALT>
 cudaError_t launch_t(const KronParams& kp, const GridArgs& g, const double* u, double* y,
                      const ChebyArgs& ch, cudaStream_t s) {
-  using Lay = K4Layout<N, NL>;
+  using Lay = K4Layout<N, NL, ALT>;
   const int planes = g.zend - g.zbeg;
   if (planes <= 0 || g.Nx <= 0 || g.Ny <= 0) return cudaSuccess;
   if (g.Ny > 65535 || planes > 65535) return cudaErrorInvalidValue;
   const dim3 grid((g.Nx + Lay::CPB - 1) / Lay::CPB, g.Ny, planes);
   const dim3 block(N, Lay::NB * Lay::CPB);
   const size_t smem = Lay::bytes();
-  auto kern = k_kron4<N, NL, MODE, OUTD>;
+  auto kern = k_kron4<N, NL, MODE, OUTD, ALT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, block, smem, s>>>(kp, g, u, y, ch);
@@ -732,13 +736,30 @@ cudaError_t launch_mode(int mode, const KronParams& kp, const GridArgs& g, const
     const char* e = std::getenv("DG_K4_OUT");
     return e ? std::atoi(e) : (N % 2 == 0 ? 1 : 0);   // measured: direct wins for even n only
   }();
+  static const int alt = [] {   // DG_K4_ALT=1: the two-lines-per-thread configuration (n = 6, 8)
+    const char* e = std::getenv("DG_K4_ALT");
+    return e ? std::atoi(e) : 0;
+  }();
+  if constexpr (K4HasAlt<N>::value) {
+    if (alt == 1) {
+      switch (mode) {
+        case KMODE_APPLY:
+          return outd ? launch_t<N, NL, KMODE_APPLY, 1, 1>(kp, g, u, y, ch, s)
+                      : launch_t<N, NL, KMODE_APPLY, 0, 1>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 1>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 1>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 1>(kp, g, u, y, ch, s);
+      }
+      return cudaErrorInvalidValue;
+    }
+  }
   switch (mode) {
     case KMODE_APPLY:
-      return outd ? launch_t<N, NL, KMODE_APPLY, 1>(kp, g, u, y, ch, s)
-                  : launch_t<N, NL, KMODE_APPLY, 0>(kp, g, u, y, ch, s);
-    case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0>(kp, g, u, y, ch, s);
-    case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0>(kp, g, u, y, ch, s);
-    case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0>(kp, g, u, y, ch, s);
+      return outd ? launch_t<N, NL, KMODE_APPLY, 1, 0>(kp, g, u, y, ch, s)
+                  : launch_t<N, NL, KMODE_APPLY, 0, 0>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 0>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 0>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 0>(kp, g, u, y, ch, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -1,0 +1,4 @@
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --workload c3 > gpurun_out/bench_q3b.json 2> gpurun_out/bench_q3b.err
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --degrees 2,5,6 > gpurun_out/bench_k4g.json 2> gpurun_out/bench_k4g.err
+timeout 600 ncu --section LaunchStats --section Occupancy --section SpeedOfLight --clock-control none -k regex:k_quad3 -s 1 -c 1 python bench.py --steps 1 --warmup 0 --quick --workload c3 > gpurun_out/ncu_q3b.log 2>&1
+echo done
