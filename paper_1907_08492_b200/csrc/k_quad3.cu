@@ -60,12 +60,14 @@ struct Q3Layout {
   static constexpr int CPB = Q3C<N>::CPB;
   static constexpr Lay3 ZY = Q3C<N>::ZY, YX = Q3C<N>::YX;
   static constexpr int S = imax3(ZY.CS, YX.CS);
-  static constexpr int PG = N;                 // face row pitch
+  static constexpr int PG = N | 1;             // face row pitch (odd: spreads banks)
   static constexpr int FP = N * PG;            // one face field (n x n)
+  // per-cell strides padded off multiples of 16 doubles (jobs of several cells share a warp)
+  static constexpr int pad16(int x) { return (x % 16 == 0) ? x + 4 : x; }
   // FA: (Z->Y) FZ[s][3] + GYn[f][3];  (X->YT) PY[f][3] + QZm[s][3]
-  static constexpr int FAC = 12 * FP;
+  static constexpr int FAC = pad16(12 * FP);
   // FB: (Y->X) FY[f][4] + FZm[s][4];  (YT->ZT) QZo[s][2]
-  static constexpr int FBC = 16 * FP;
+  static constexpr int FBC = pad16(16 * FP);
   // x-halo: per block edge h: HZ[3] (Z->Y) and HXo[4] (Y->X)
   static constexpr int HXC = 7 * FP;
   static constexpr int doubles() { return CPB * (3 * S + FAC + FBC) + 2 * HXC; }
@@ -474,12 +476,29 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
       eo_apply<N, 1>(qp.S, c3, gz);
       const double* Gp = ga.G + cid * (6 * N3) + (xq2 * N + xq1) * N;
       const double wyz = qp.w[xq1] * qp.w[xq2];
+      double Gl[GEOM == GEOM_PER_QPOINT ? 6 : 1][N];
+      if constexpr (GEOM == GEOM_PER_QPOINT) {   // the x-line's tensors: contiguous runs of n
+#pragma unroll
+        for (int m = 0; m < 6; ++m) {
+          if constexpr (N % 2 == 0) {
+#pragma unroll
+            for (int k = 0; k < N; k += 2) {
+              const double2 v = __ldg(reinterpret_cast<const double2*>(Gp + m * N3 + k));
+              Gl[m][k] = v.x;
+              Gl[m][k + 1] = v.y;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < N; ++k) Gl[m][k] = __ldg(Gp + m * N3 + k);
+          }
+        }
+      }
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         double G[6];
         if constexpr (GEOM == GEOM_PER_QPOINT) {
 #pragma unroll
-          for (int m = 0; m < 6; ++m) G[m] = __ldg(Gp + m * N3 + k);
+          for (int m = 0; m < 6; ++m) G[m] = Gl[m][k];
         } else {
           const double wq = wyz * qp.w[k];
 #pragma unroll
