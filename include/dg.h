@@ -165,6 +165,31 @@ dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* wor
                               int32_t degree, double lambda_max, double lo_frac,
                               double hi_frac, int32_t inner, void* stream);
 
+/* ---------------------------------------------------------------- solver layer
+ * (PAPER.md:1811-1832).  All vectors are device, n_local_dofs
+ * long; dot products are global over the z-slabs (ncclAllReduce when nranks > 1; the
+ * external-transport mode returns DG_ERR_UNSUPPORTED).  These calls synchronise `stream`. */
+
+/* z = P^{-1} r, the inner preconditioner of dg_chebyshev_smooth (DG_INNER_*). */
+dg_status dg_apply_preconditioner(dg_mesh m, int32_t inner, const double* r, double* z, void* stream);
+
+/* *out (host) = a . b over all ranks (deterministic two-level reduction). */
+dg_status dg_dot(dg_mesh m, const double* a, const double* b, double* out, void* stream);
+
+/* lambda_max(P^{-1} A) from `iters` (1..200) Lanczos steps started from the vector
+ * [-5.5, -4.5, ..., 5.5] repeated over the global DoF index (the
+ * paper uses 15).  Largest eigenvalue of the Lanczos tridiagonal. */
+dg_status dg_lanczos_lambda_max(dg_mesh m, int32_t inner, int32_t iters, double* lambda_max, void* stream);
+
+/* Conjugate gradients preconditioned by one degree-`cheby_degree` Chebyshev sweep from a
+ * zero initial guess (range [lo_frac, hi_frac] * lambda_max, inner preconditioner `inner`):
+ * a fixed symmetric polynomial preconditioner.  x: in initial guess, out iterate.  Stops
+ * when ||r_k|| <= rel_tol ||r_0|| or after max_iter iterations; *iters and *rel_res
+ * (host, may be NULL) report the outcome.  DG_ERR_NUMERIC on breakdown (p.Ap <= 0). */
+dg_status dg_pcg(dg_mesh m, const double* b, double* x, double rel_tol, int32_t max_iter,
+                 int32_t cheby_degree, double lambda_max, double lo_frac, double hi_frac, int32_t inner,
+                 int32_t* iters, double* rel_res, void* stream);
+
 /* Inverse of the inner preconditioner's diagonal, copied to `out` (device,
  * n_local_dofs): diag(A_GL)^{-1} (GL_JACOBI) or diag(A)^{-1} (POINT_JACOBI). */
 dg_status dg_inverse_diagonal(dg_mesh m, int32_t inner, double* out, void* stream);

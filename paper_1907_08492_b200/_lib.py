@@ -62,6 +62,16 @@ SYMBOLS = {
     "dg_halo_set": (ctypes.c_int, [ctypes.c_void_p] * 4),
     "dg_tables_1d": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                     ctypes.c_void_p, ctypes.c_int64]),
+    "dg_apply_preconditioner": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                                               ctypes.c_void_p, ctypes.c_void_p]),
+    "dg_dot": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]),
+    "dg_lanczos_lambda_max": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]),
+    "dg_pcg": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                              ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                              ctypes.c_double, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                              ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]),
 }
 
 _lib = None

@@ -234,6 +234,41 @@ class Mesh:
                                          _stream(stream)), "dg_chebyshev_smooth")
         return x
 
+    def apply_preconditioner(self, r, z=None, inner="gl_jacobi", stream=None):
+        """z = P^{-1} r for the inner preconditioner of the smoother (Eq. (12) / FDM)."""
+        if z is None:
+            z = self.empty()
+        _check(lib().dg_apply_preconditioner(self._h, INNER[inner], _ptr(r, self.n_local_dofs, "r"),
+                                             _ptr(z, self.n_local_dofs, "z"), _stream(stream)),
+               "dg_apply_preconditioner")
+        return z
+
+    def dot(self, a, b, stream=None) -> float:
+        """Global (all-rank) dot product on the GPU, deterministic two-level reduction."""
+        out = ctypes.c_double()
+        _check(lib().dg_dot(self._h, _ptr(a, self.n_local_dofs, "a"), _ptr(b, self.n_local_dofs, "b"),
+                            ctypes.byref(out), _stream(stream)), "dg_dot")
+        return out.value
+
+    def lanczos_lambda_max(self, inner="gl_jacobi", iters=15, stream=None) -> float:
+        """lambda_max(P^{-1}A) from `iters` Lanczos steps."""
+        out = ctypes.c_double()
+        _check(lib().dg_lanczos_lambda_max(self._h, INNER[inner], int(iters), ctypes.byref(out),
+                                           _stream(stream)), "dg_lanczos_lambda_max")
+        return out.value
+
+    def pcg(self, b, x, lambda_max, rel_tol=1e-9, max_iter=500, cheby_degree=5, lo=0.06, hi=1.2,
+            inner="gl_jacobi", stream=None):
+        """CG with the Chebyshev sweep as preconditioner; x: in initial guess, out solution.
+        Returns (iterations, relative residual)."""
+        it = ctypes.c_int32()
+        rr = ctypes.c_double()
+        _check(lib().dg_pcg(self._h, _ptr(b, self.n_local_dofs, "b"), _ptr(x, self.n_local_dofs, "x"),
+                            float(rel_tol), int(max_iter), int(cheby_degree), float(lambda_max), float(lo),
+                            float(hi), INNER[inner], ctypes.byref(it), ctypes.byref(rr), _stream(stream)),
+               "dg_pcg")
+        return it.value, rr.value
+
     def inverse_diagonal(self, inner="gl_jacobi", out=None, stream=None):
         if out is None:
             out = self.empty()

@@ -215,6 +215,7 @@ struct dg_mesh_s {
   int rank = 0, nranks = 1;
   int64_t launches = 0;
   bool fdm_ok = false;            // FDM tables built (Cartesian meshes)
+  double* d_dot = nullptr;        // dot-product scratch: partials + result
 };
 
 namespace {
@@ -649,6 +650,7 @@ dg_status dg_mesh_destroy(dg_mesh m) {
   cudaFree(m->d_jinv);
   cudaFree(m->d_dinv_gl);
   cudaFree(m->d_dinv_pj);
+  cudaFree(m->d_dot);
   cudaFree(m->d_recv_lo);
   cudaFree(m->d_recv_hi);
   cudaFree(m->d_send_lo);
@@ -933,3 +935,214 @@ dg_status run_pass(dg_mesh m, int mode, bool kron, const double* u, double* y, c
 }
 
 }  // namespace
+
+// ================================================================ solvers (NEXT#4)
+// GPU Lanczos estimate of lambda_max(P^{-1}A) and preconditioned CG with the Chebyshev
+// sweep as preconditioner.
+namespace {
+
+dg_status pinv_impl(dg_mesh m, int inner, const double* r, double* z, cudaStream_t s) {
+  if (inner == DG_INNER_FDM) {
+    if (!m->fdm_ok) return fail(DG_ERR_UNSUPPORTED, "DG_INNER_FDM needs a Cartesian mesh");
+    return post_launch(m, launch_pinv(m->n, DG_INNER_FDM, m->kp, r, nullptr, z, m->ncells_local, s), "pinv", s);
+  }
+  const bool gl = inner == DG_INNER_GL_JACOBI && m->desc.basis == DG_BASIS_HERMITE_LIKE;
+  double** dsrc = gl ? &m->d_dinv_gl : &m->d_dinv_pj;
+  dg_status st = build_diag(m, inner == DG_INNER_GL_JACOBI, dsrc, s);
+  if (st != DG_OK) return st;
+  return post_launch(m, launch_pinv(m->n, gl ? DG_INNER_GL_JACOBI : DG_INNER_POINT_JACOBI, m->kp, r, *dsrc, z,
+                                    m->ncells_local, s), "pinv", s);
+}
+
+dg_status dot_impl(dg_mesh m, const double* a, const double* b, double* out, cudaStream_t s) {
+  if (!m->d_dot) CUDA_TRY(cudaMalloc(&m->d_dot, sizeof(double) * (dot_partials() + 1)));
+  double* res = m->d_dot + dot_partials();
+  dg_status st = post_launch(m, launch_dot(a, b, m->ndofs_local, m->d_dot, res, s), "dot", s);
+  if (st != DG_OK) return st;
+  m->launches++;   // two kernels
+  if (m->nranks > 1) {
+    if (!m->comm) return fail(DG_ERR_UNSUPPORTED, "global dot products need the NCCL communicator");
+    NCCL_TRY(ncclAllReduce(res, res, 1, ncclDouble, ncclSum, m->comm, s));
+  }
+  CUDA_TRY(cudaMemcpyAsync(out, res, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return DG_OK;
+}
+
+dg_status axpby(dg_mesh m, double a, const double* x, double b, double* y, cudaStream_t s) {
+  return post_launch(m, launch_axpby(a, x, b, y, m->ndofs_local, s), "axpby", s);
+}
+
+// largest eigenvalue of the symmetric tridiagonal (alpha, beta) by cyclic Jacobi
+double tridiag_max_eig(const std::vector<double>& al, const std::vector<double>& be) {
+  const int k = (int)al.size();
+  std::vector<long double> A((size_t)k * k, 0.0L);
+  for (int i = 0; i < k; ++i) {
+    A[i * k + i] = al[i];
+    if (i + 1 < k) A[i * k + i + 1] = A[(i + 1) * k + i] = be[i];
+  }
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    long double off = 0;
+    for (int p = 0; p < k; ++p)
+      for (int q = p + 1; q < k; ++q) off += A[p * k + q] * A[p * k + q];
+    if (off < 1e-60L) break;
+    for (int p = 0; p < k; ++p)
+      for (int q = p + 1; q < k; ++q) {
+        if (A[p * k + q] == 0) continue;
+        const long double th = (A[q * k + q] - A[p * k + p]) / (2 * A[p * k + q]);
+        const long double t = (th >= 0 ? 1 : -1) / (std::fabs(th) + std::sqrt(th * th + 1));
+        const long double c = 1 / std::sqrt(t * t + 1), sn = t * c;
+        for (int r = 0; r < k; ++r) {
+          const long double ap = A[r * k + p], aq = A[r * k + q];
+          A[r * k + p] = c * ap - sn * aq;
+          A[r * k + q] = sn * ap + c * aq;
+        }
+        for (int r = 0; r < k; ++r) {
+          const long double ap = A[p * k + r], aq = A[q * k + r];
+          A[p * k + r] = c * ap - sn * aq;
+          A[q * k + r] = sn * ap + c * aq;
+        }
+      }
+  }
+  long double mx = A[0];
+  for (int i = 1; i < k; ++i) mx = std::max(mx, A[i * k + i]);
+  return (double)mx;
+}
+
+struct DevVecs {
+  std::vector<double*> v;
+  ~DevVecs() {
+    for (double* p : v) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+dg_status dg_apply_preconditioner(dg_mesh m, int32_t inner, const double* r, double* z, void* stream) {
+  if (!m || !r || !z) return fail(DG_ERR_PARAM, "NULL argument");
+  if (inner != DG_INNER_GL_JACOBI && inner != DG_INNER_POINT_JACOBI && inner != DG_INNER_FDM)
+    return fail(DG_ERR_PARAM, "bad inner %d", inner);
+  return pinv_impl(m, inner, r, z, (cudaStream_t)stream);
+}
+
+dg_status dg_dot(dg_mesh m, const double* a, const double* b, double* out, void* stream) {
+  if (!m || !a || !b || !out) return fail(DG_ERR_PARAM, "NULL argument");
+  return dot_impl(m, a, b, out, (cudaStream_t)stream);
+}
+
+dg_status dg_lanczos_lambda_max(dg_mesh m, int32_t inner, int32_t iters, double* lambda_max, void* stream) {
+  if (!m || !lambda_max) return fail(DG_ERR_PARAM, "NULL argument");
+  if (iters < 1 || iters > 200) return fail(DG_ERR_PARAM, "iters %d not in 1..200", iters);
+  if (inner != DG_INNER_GL_JACOBI && inner != DG_INNER_POINT_JACOBI && inner != DG_INNER_FDM)
+    return fail(DG_ERR_PARAM, "bad inner %d", inner);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nd = m->ndofs_local;
+  DevVecs w;
+  for (int i = 0; i < 5; ++i) {
+    double* p = nullptr;
+    CUDA_TRY(cudaMalloc(&p, sizeof(double) * (size_t)std::max<int64_t>(nd, 1)));
+    w.v.push_back(p);
+  }
+  double *v = w.v[0], *vp = w.v[1], *z = w.v[2], *ww = w.v[3], *wz = w.v[4];
+  const int64_t plane_dofs = (int64_t)m->N[0] * m->N[1] * m->n * m->n * m->n;
+  dg_status st = post_launch(m, launch_lanczos_start(v, nd, (int64_t)m->z_begin * plane_dofs, s), "lanczos", s);
+  if (st != DG_OK) return st;
+  if ((st = pinv_impl(m, inner, v, z, s)) != DG_OK) return st;
+  double vz;
+  if ((st = dot_impl(m, v, z, &vz, s)) != DG_OK) return st;
+  if (!(vz > 0)) return fail(DG_ERR_NUMERIC, "P^-1 not positive definite in Lanczos");
+  double beta = std::sqrt(vz);
+  if ((st = axpby(m, 0.0, v, 1.0 / beta, v, s)) != DG_OK) return st;
+  if ((st = axpby(m, 0.0, z, 1.0 / beta, z, s)) != DG_OK) return st;
+  CUDA_TRY(cudaMemsetAsync(vp, 0, sizeof(double) * (size_t)nd, s));
+  std::vector<double> al, be;
+  double b_prev = 0.0;
+  ChebyArgs none{};
+  for (int it = 0; it < iters; ++it) {
+    if ((st = run_pass(m, KMODE_APPLY, m->cartesian, z, ww, none, false, s)) != DG_OK) return st;
+    double a;
+    if ((st = dot_impl(m, ww, z, &a, s)) != DG_OK) return st;
+    if ((st = axpby(m, -a, v, 1.0, ww, s)) != DG_OK) return st;
+    if ((st = axpby(m, -b_prev, vp, 1.0, ww, s)) != DG_OK) return st;
+    if ((st = pinv_impl(m, inner, ww, wz, s)) != DG_OK) return st;
+    double wwz;
+    if ((st = dot_impl(m, ww, wz, &wwz, s)) != DG_OK) return st;
+    const double b = std::sqrt(std::max(wwz, 0.0));
+    al.push_back(a);
+    if (b < 1e-300) break;
+    be.push_back(b);
+    std::swap(vp, v);                      // v_prev <- v
+    if ((st = axpby(m, 1.0 / b, ww, 0.0, v, s)) != DG_OK) return st;   // v <- w / b
+    if ((st = axpby(m, 1.0 / b, wz, 0.0, z, s)) != DG_OK) return st;   // z <- wz / b
+    b_prev = b;
+  }
+  *lambda_max = tridiag_max_eig(al, be);
+  return DG_OK;
+}
+
+dg_status dg_pcg(dg_mesh m, const double* b, double* x, double rel_tol, int32_t max_iter, int32_t cheby_degree,
+                 double lambda_max, double lo_frac, double hi_frac, int32_t inner, int32_t* iters, double* rel_res,
+                 void* stream) {
+  if (!m || !b || !x) return fail(DG_ERR_PARAM, "NULL argument");
+  if (max_iter < 0 || cheby_degree < 1) return fail(DG_ERR_PARAM, "max_iter < 0 or cheby_degree < 1");
+  if (b == x) return fail(DG_ERR_PARAM, "b and x must not alias");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nd = m->ndofs_local;
+  DevVecs w;
+  for (int i = 0; i < 4; ++i) {
+    double* p = nullptr;
+    CUDA_TRY(cudaMalloc(&p, sizeof(double) * (size_t)std::max<int64_t>(nd, 1)));
+    w.v.push_back(p);
+  }
+  double* work2 = nullptr;
+  CUDA_TRY(cudaMalloc(&work2, sizeof(double) * (size_t)std::max<int64_t>(2 * nd, 1)));
+  w.v.push_back(work2);
+  double *r = w.v[0], *z = w.v[1], *p = w.v[2], *q = w.v[3];
+  ChebyArgs none{};
+  auto precond = [&](const double* rin, double* zout) -> dg_status {   // z = Chebyshev sweep from 0
+    CUDA_TRY(cudaMemsetAsync(zout, 0, sizeof(double) * (size_t)nd, s));
+    return dg_chebyshev_smooth(m, rin, zout, work2, cheby_degree, lambda_max, lo_frac, hi_frac, inner, s);
+  };
+  dg_status st;
+  // r = b - A x
+  if ((st = run_pass(m, KMODE_APPLY, m->cartesian, x, r, none, false, s)) != DG_OK) return st;
+  if ((st = axpby(m, 1.0, b, -1.0, r, s)) != DG_OK) return st;
+  double rr0;
+  if ((st = dot_impl(m, r, r, &rr0, s)) != DG_OK) return st;
+  const double r0 = std::sqrt(rr0);
+  double res = r0 > 0 ? 1.0 : 0.0;
+  int k = 0;
+  if (r0 > 0 && max_iter > 0) {
+    if ((st = precond(r, z)) != DG_OK) return st;
+    CUDA_TRY(cudaMemcpyAsync(p, z, sizeof(double) * (size_t)nd, cudaMemcpyDeviceToDevice, s));
+    double rz;
+    if ((st = dot_impl(m, r, z, &rz, s)) != DG_OK) return st;
+    for (k = 1; k <= max_iter; ++k) {
+      if ((st = run_pass(m, KMODE_APPLY, m->cartesian, p, q, none, false, s)) != DG_OK) return st;
+      double pq;
+      if ((st = dot_impl(m, p, q, &pq, s)) != DG_OK) return st;
+      if (!(pq > 0)) return fail(DG_ERR_NUMERIC, "CG breakdown: p.Ap = %g", pq);
+      const double alpha = rz / pq;
+      if ((st = axpby(m, alpha, p, 1.0, x, s)) != DG_OK) return st;
+      if ((st = axpby(m, -alpha, q, 1.0, r, s)) != DG_OK) return st;
+      double rr;
+      if ((st = dot_impl(m, r, r, &rr, s)) != DG_OK) return st;
+      res = std::sqrt(rr) / r0;
+      if (res <= rel_tol || k == max_iter) break;
+      if ((st = precond(r, z)) != DG_OK) return st;
+      double rz_new;
+      if ((st = dot_impl(m, r, z, &rz_new, s)) != DG_OK) return st;
+      const double beta = rz_new / rz;
+      if ((st = axpby(m, 1.0, z, beta, p, s)) != DG_OK) return st;   // p = z + beta p
+      rz = rz_new;
+    }
+    if (k > max_iter) k = max_iter;
+  }
+  if (iters) *iters = k;
+  if (rel_res) *rel_res = res;
+  return DG_OK;
+}
+
+}  // extern "C"

@@ -137,6 +137,13 @@ bool quad3_supported(int n, int geom);
 cudaError_t launch_quad3(int n, int NL, int geom, int mode, const QuadParams& qp, const GeomArgs& ga,
                          const GridArgs& g, const double* u, double* y, const ChebyArgs& ch,
                          cudaStream_t s);
+// solver kernels (k_solver.cu): standalone P^{-1}, deterministic dot, vector updates
+cudaError_t launch_pinv(int n, int inner, const KronParams& kp, const double* r, const double* dinv, double* z,
+                        int64_t ncells, cudaStream_t s);
+int dot_partials();
+cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* part, double* out, cudaStream_t s);
+cudaError_t launch_axpby(double alpha, const double* x, double beta, double* y, int64_t n, cudaStream_t s);
+cudaError_t launch_lanczos_start(double* v, int64_t n, int64_t g0, cudaStream_t s);
 cudaError_t launch_geom_qpoint(int n, const MapParams& mp, int Nx, int Ny, int nz, double* G,
                                double* face[3], int* err_flag, cudaStream_t s);
 // diagonal of the operator in a basis given by tables (S, DS, v0, v1, d0, d1 at the

@@ -251,3 +251,108 @@ def test_c4_full_size_sampled(p):
     del y
     ref = _oracle(spec).apply(uh, cells=cells).reshape(len(cells), -1)
     assert np.abs(yh - ref).max() <= TOL * np.abs(ref).max()
+
+
+# ---------------------------------------------------------------- solver layer (NEXT#4)
+def _small_mesh(p=3, seed=80):
+    return MeshSpec(degree=p, n_cells=(3, 2, 3), bc=("dirichlet", "periodic", "dirichlet"), seed=seed)
+
+
+def test_gpu_dot_matches_numpy():
+    _needs_gpu()
+    spec = c4_spec(2)
+    m = _gpu_mesh(spec)
+    a = uniform_vector(m.n_local_dofs, 1)
+    b = uniform_vector(m.n_local_dofs, 2)
+    ref = float(np.dot(a, b))
+    assert abs(m.dot(_dev(a), _dev(b)) - ref) <= 1e-12 * np.sqrt(np.dot(a, a) * np.dot(b, b))
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+@pytest.mark.parametrize("inner", ["gl_jacobi", "point_jacobi", "fdm"])
+def test_gpu_apply_preconditioner(p, inner):
+    _needs_gpu()
+    from oracle import fdm
+    from oracle import smoother as sm
+    from oracle.geometry import mesh_from_spec
+    from oracle.sipg import SIPG
+    spec = _small_mesh(p)
+    om = mesh_from_spec(spec)
+    if inner == "gl_jacobi":
+        P = sm.GLJacobi(SIPG(om, p, "gl"))
+    elif inner == "point_jacobi":
+        P = sm.PointJacobi(SIPG(om, p))
+    else:
+        P = fdm.FDM(p, (1 / 3, 1 / 2, 1 / 3))
+    r = uniform_vector(spec.n_dofs, 90 + p)
+    m = _gpu_mesh(spec)
+    z = m.apply_preconditioner(_dev(r), inner=inner).cpu().numpy()
+    assert _rel(z, P(r)) <= TOL
+
+
+@pytest.mark.parametrize("p,inner", [(3, "gl_jacobi"), (5, "gl_jacobi"), (4, "fdm"), (2, "point_jacobi")])
+def test_gpu_lanczos_matches_oracle(p, inner):
+    _needs_gpu()
+    from oracle import fdm
+    from oracle import smoother as sm
+    from oracle.geometry import mesh_from_spec
+    from oracle.sipg import SIPG
+    spec = _small_mesh(p)
+    om = mesh_from_spec(spec)
+    H = SIPG(om, p)
+    P = {"gl_jacobi": lambda: sm.GLJacobi(SIPG(om, p, "gl")), "point_jacobi": lambda: sm.PointJacobi(H),
+         "fdm": lambda: fdm.FDM(p, (1 / 3, 1 / 2, 1 / 3))}[inner]()
+    ref = sm.lanczos_lambda_max(H.apply, P, spec.n_dofs, iters=15)
+    m = _gpu_mesh(spec)
+    assert abs(m.lanczos_lambda_max(inner=inner, iters=15) - ref) <= 1e-10 * ref
+
+
+def test_gpu_lanczos_c1_sanity_value():
+    """lambda_max(P^-1 A_H) for C1 (p=3, 4^3) is 2.592367.  A Lanczos Ritz
+    value approaches lambda_max from below; 15 steps land within a few per cent."""
+    _needs_gpu()
+    m = _gpu_mesh(CONFIGS["C1"])
+    est = m.lanczos_lambda_max("gl_jacobi", 15)
+    assert 0.97 * 2.592367 <= est <= 2.592367 * (1 + 1e-9)
+
+
+@pytest.mark.parametrize("inner,k", [("gl_jacobi", 3), ("fdm", 4)])
+def test_gpu_pcg_iterates_match_oracle(inner, k):
+    _needs_gpu()
+    from oracle import fdm
+    from oracle import smoother as sm
+    from oracle import solver
+    from oracle.geometry import mesh_from_spec
+    from oracle.sipg import SIPG
+    p = 3
+    spec = _small_mesh(p)
+    om = mesh_from_spec(spec)
+    H = SIPG(om, p)
+    P = sm.GLJacobi(SIPG(om, p, "gl")) if inner == "gl_jacobi" else fdm.FDM(p, (1 / 3, 1 / 2, 1 / 3))
+    lmax = 2.5
+    M = lambda r: sm.chebyshev(H.apply, P, r, np.zeros_like(r), 3, lmax)   # noqa: E731
+    b = uniform_vector(spec.n_dofs, 91)
+    x0 = uniform_vector(spec.n_dofs, 92)
+    xr, itr, resr = solver.pcg(H.apply, M, b, x0, rel_tol=0.0, max_iter=k)
+    m = _gpu_mesh(spec)
+    x = _dev(x0)
+    it, res = m.pcg(_dev(b), x, lmax, rel_tol=0.0, max_iter=k, cheby_degree=3, inner=inner)
+    assert it == itr == k
+    assert _rel(x.cpu().numpy(), xr) <= 1e-10
+    assert abs(res - resr) <= 1e-8 * resr
+
+
+def test_gpu_pcg_solves():
+    _needs_gpu()
+    from oracle.geometry import mesh_from_spec
+    from oracle.sipg import SIPG
+    spec = MeshSpec(degree=3, n_cells=(2, 2, 3), seed=5)
+    A = SIPG(mesh_from_spec(spec), 3).assemble()
+    b = uniform_vector(spec.n_dofs, 9)
+    xs = np.linalg.solve(A, b)
+    m = _gpu_mesh(spec)
+    lmax = m.lanczos_lambda_max("gl_jacobi", 15)
+    x = torch.zeros(spec.n_dofs, dtype=torch.float64, device="cuda")
+    it, res = m.pcg(_dev(b), x, lmax, rel_tol=1e-11, max_iter=200, cheby_degree=3)
+    assert res <= 1e-11 and it < 60
+    assert _rel(x.cpu().numpy(), xs) <= 1e-9
