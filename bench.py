@@ -404,6 +404,33 @@ def run_ours(a, rank, world, local_rank):
             nd, cd = s["n_global"], a.cheby_degree
             ops[s["key"]]["cheby_fdm_step_dofs_per_s"] = nd * cd * a.steps / (ms * 1e-3)
             ops[s["key"]]["cheby_fdm_sweep_gbs"] = nd * (24.0 + 32.0 * (cd - 1)) * a.steps / (ms * 1e-3) / 1e9
+    # ---------------------------------------------------------------- fp32 path (extra)
+    # the same matvec and GL-Jacobi Chebyshev sweep in fp32 (8 B/DoF
+    # per vector access: matvec 8 B/DoF, Chebyshev step 20 B/DoF); after the timed region,
+    # not part of `value`.
+    if a.workload in ("c4", "c5") and not a.quick and world == 1:
+        for s in setups:
+            m_ = s["m"]
+            u32, b32 = s["u"].float(), s["b"].float()
+            y32 = torch.empty_like(u32)
+            x32 = torch.zeros_like(u32)
+            w32 = torch.empty(2 * u32.numel(), dtype=torch.float32, device=dev)
+            m_.apply_laplace_f32(u32, y32)
+            m_.chebyshev_smooth_f32(b32, x32, s["lmax"], degree=a.cheby_degree, work2=w32)
+            barrier()
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            e[0].record(stream)
+            for _ in range(a.steps):
+                m_.apply_laplace_f32(u32, y32)
+            e[1].record(stream)
+            for _ in range(a.steps):
+                m_.chebyshev_smooth_f32(b32, x32, s["lmax"], degree=a.cheby_degree, work2=w32)
+            e[2].record(stream)
+            barrier()
+            nd, cd = s["n_global"], a.cheby_degree
+            ops[s["key"]]["matvec_f32_dofs_per_s"] = nd * a.steps / (e[0].elapsed_time(e[1]) * 1e-3)
+            ops[s["key"]]["cheby_f32_step_dofs_per_s"] = nd * cd * a.steps / (e[1].elapsed_time(e[2]) * 1e-3)
+            del u32, b32, y32, x32, w32
     # ---------------------------------------------------------------- e2e (host buffers)
     if not a.no_e2e and not a.quick:
         h2d = d2h = 0

@@ -190,6 +190,16 @@ dg_status dg_pcg(dg_mesh m, const double* b, double* x, double rel_tol, int32_t 
                  int32_t cheby_degree, double lambda_max, double lo_frac, double hi_frac, int32_t inner,
                  int32_t* iters, double* rel_res, void* stream);
 
+/* ---------------------------------------------------------------- fp32 path
+ * (the paper's smoothers run in fp32).
+ * Same operator and smoother as the fp64 calls with float vectors: the 1D tables are
+ * rounded to float once, every contraction and the update run in fp32.  Cartesian meshes
+ * (degree 2..8, k_kron4 path) on a single z-slab only; DG_ERR_UNSUPPORTED otherwise. */
+dg_status dg_apply_laplace_f32(dg_mesh m, const float* u, float* y, void* stream);
+dg_status dg_chebyshev_smooth_f32(dg_mesh m, const float* b, float* x, float* work2, int32_t degree,
+                                  double lambda_max, double lo_frac, double hi_frac, int32_t inner,
+                                  void* stream);
+
 /* Inverse of the inner preconditioner's diagonal, copied to `out` (device,
  * n_local_dofs): diag(A_GL)^{-1} (GL_JACOBI) or diag(A)^{-1} (POINT_JACOBI). */
 dg_status dg_inverse_diagonal(dg_mesh m, int32_t inner, double* out, void* stream);

@@ -44,9 +44,10 @@ def _stream(stream):
     return ctypes.c_void_p(int(stream))
 
 
-def _ptr(t, n=None, name="tensor"):
-    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda:
-        raise TypeError(f"{name} must be a CUDA float64 tensor")
+def _ptr(t, n=None, name="tensor", dtype=None):
+    dtype = torch.float64 if dtype is None else dtype
+    if not isinstance(t, torch.Tensor) or t.dtype != dtype or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA {dtype} tensor")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
     if n is not None and t.numel() < n:
@@ -214,6 +215,28 @@ class Mesh:
                                       _ptr(y, self.n_local_dofs, "y"), int(flags), _stream(stream)),
                "dg_apply_laplace")
         return y
+
+    def apply_laplace_f32(self, u, y=None, stream=None):
+        """y = A u in single precision (Cartesian meshes, single slab; SURVEY.md §8(f) NEXT#3)."""
+        f32 = torch.float32
+        if y is None:
+            y = torch.empty(self.n_local_dofs, dtype=f32, device="cuda")
+        _check(lib().dg_apply_laplace_f32(self._h, _ptr(u, self.n_local_dofs, "u", f32),
+                                          _ptr(y, self.n_local_dofs, "y", f32), _stream(stream)),
+               "dg_apply_laplace_f32")
+        return y
+
+    def chebyshev_smooth_f32(self, b, x, lambda_max, degree=5, lo=0.06, hi=1.2, inner="gl_jacobi",
+                             work2=None, stream=None):
+        f32 = torch.float32
+        if work2 is None:
+            work2 = torch.empty(2 * self.n_local_dofs, dtype=f32, device="cuda")
+        _check(lib().dg_chebyshev_smooth_f32(self._h, _ptr(b, self.n_local_dofs, "b", f32),
+                                             _ptr(x, self.n_local_dofs, "x", f32),
+                                             _ptr(work2, 2 * self.n_local_dofs, "work2", f32), int(degree),
+                                             float(lambda_max), float(lo), float(hi), INNER[inner],
+                                             _stream(stream)), "dg_chebyshev_smooth_f32")
+        return x
 
     def basis_change(self, op, x, out=None, stream=None):
         if out is None:

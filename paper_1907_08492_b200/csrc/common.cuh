@@ -20,44 +20,43 @@ namespace dgb {
 constexpr int eo_size(int n) { return 2 * (n / 2) * (n / 2) + 2 * (n / 2) + 1; }
 constexpr int kEO = 41;   // eo_size(9): enough for n <= 9
 
-template <int N>
+template <int N, typename T = double>
 struct EOSplit {
   static constexpr int H = N / 2;
-  double e[H > 0 ? H : 1], o[H > 0 ? H : 1], m;
+  T e[H > 0 ? H : 1], o[H > 0 ? H : 1], m;
 };
 
-template <int N>
-__device__ __forceinline__ EOSplit<N> eo_split(const double (&x)[N]) {
-  EOSplit<N> s;
+template <int N, typename T>
+__device__ __forceinline__ EOSplit<N, T> eo_split(const T (&x)[N]) {
+  EOSplit<N, T> s;
 #pragma unroll
   for (int j = 0; j < N / 2; ++j) {
     s.e[j] = x[j] + x[N - 1 - j];
     s.o[j] = x[j] - x[N - 1 - j];
   }
-  s.m = (N & 1) ? x[N / 2] : 0.0;
+  s.m = (N & 1) ? x[N / 2] : T(0);
   return s;
 }
 
 // y (=|+=) A x from the split of x.  S = reflection parity of A.
-template <int N, int S, bool ACC>
-__device__ __forceinline__ void eo_mul(const double* __restrict__ A, const EOSplit<N>& s,
-                                       double (&y)[N]) {
+template <int N, int S, bool ACC, typename T>
+__device__ __forceinline__ void eo_mul(const T* __restrict__ A, const EOSplit<N, T>& s, T (&y)[N]) {
   constexpr int H = N / 2;
-  const double* E = A;
-  const double* O = A + H * H;
-  const double* C = A + 2 * H * H;
-  const double* R = A + 2 * H * H + H;
+  const T* E = A;
+  const T* O = A + H * H;
+  const T* C = A + 2 * H * H;
+  const T* R = A + 2 * H * H + H;
 #pragma unroll
   for (int i = 0; i < H; ++i) {
-    double ye = 0.0, yo = 0.0;
+    T ye = T(0), yo = T(0);
     if (N & 1) ye = C[i] * s.m;
 #pragma unroll
     for (int j = 0; j < H; ++j) {
       ye = fma(E[i * H + j], s.e[j], ye);
       yo = fma(O[i * H + j], s.o[j], yo);
     }
-    const double lo = ye + yo;
-    const double hi = (S > 0) ? (ye - yo) : (yo - ye);
+    const T lo = ye + yo;
+    const T hi = (S > 0) ? (ye - yo) : (yo - ye);
     if (ACC) {
       y[i] += lo;
       y[N - 1 - i] += hi;
@@ -67,7 +66,7 @@ __device__ __forceinline__ void eo_mul(const double* __restrict__ A, const EOSpl
     }
   }
   if (N & 1) {
-    double ym = (S > 0) ? R[H] * s.m : 0.0;
+    T ym = (S > 0) ? R[H] * s.m : T(0);
 #pragma unroll
     for (int j = 0; j < H; ++j) ym = fma(R[j], (S > 0) ? s.e[j] : s.o[j], ym);
     if (ACC)
@@ -78,14 +77,13 @@ __device__ __forceinline__ void eo_mul(const double* __restrict__ A, const EOSpl
 }
 
 // y = A1 x1 + A2 x2 (both parity S) with one recombination of the even/odd halves
-template <int N, int S>
-__device__ __forceinline__ void eo_mul2(const double* __restrict__ A1, const EOSplit<N>& s1,
-                                        const double* __restrict__ A2, const EOSplit<N>& s2,
-                                        double (&y)[N]) {
+template <int N, int S, typename T>
+__device__ __forceinline__ void eo_mul2(const T* __restrict__ A1, const EOSplit<N, T>& s1,
+                                        const T* __restrict__ A2, const EOSplit<N, T>& s2, T (&y)[N]) {
   constexpr int H = N / 2;
 #pragma unroll
   for (int i = 0; i < H; ++i) {
-    double ye = 0.0, yo = 0.0;
+    T ye = T(0), yo = T(0);
     if (N & 1) ye = fma(A2[2 * H * H + i], s2.m, A1[2 * H * H + i] * s1.m);
 #pragma unroll
     for (int j = 0; j < H; ++j) {
@@ -101,9 +99,9 @@ __device__ __forceinline__ void eo_mul2(const double* __restrict__ A1, const EOS
     y[N - 1 - i] = (S > 0) ? (ye - yo) : (yo - ye);
   }
   if (N & 1) {
-    const double* R1 = A1 + 2 * H * H + H;
-    const double* R2 = A2 + 2 * H * H + H;
-    double ym = (S > 0) ? fma(R2[H], s2.m, R1[H] * s1.m) : 0.0;
+    const T* R1 = A1 + 2 * H * H + H;
+    const T* R2 = A2 + 2 * H * H + H;
+    T ym = (S > 0) ? fma(R2[H], s2.m, R1[H] * s1.m) : T(0);
 #pragma unroll
     for (int j = 0; j < H; ++j) {
       ym = fma(R1[j], (S > 0) ? s1.e[j] : s1.o[j], ym);
@@ -113,25 +111,22 @@ __device__ __forceinline__ void eo_mul2(const double* __restrict__ A1, const EOS
   }
 }
 
-template <int N, int S>
-__device__ __forceinline__ void eo_apply(const double* __restrict__ A, const double (&x)[N],
-                                         double (&y)[N]) {
+template <int N, int S, typename T>
+__device__ __forceinline__ void eo_apply(const T* __restrict__ A, const T (&x)[N], T (&y)[N]) {
   eo_mul<N, S, false>(A, eo_split<N>(x), y);
 }
 
-template <int N, int S>
-__device__ __forceinline__ void eo_apply_add(const double* __restrict__ A, const double (&x)[N],
-                                             double (&y)[N]) {
+template <int N, int S, typename T>
+__device__ __forceinline__ void eo_apply_add(const T* __restrict__ A, const T (&x)[N], T (&y)[N]) {
   eo_mul<N, S, true>(A, eo_split<N>(x), y);
 }
 
 // Dense n x n (row-major, parameter space) times a short vector: y[i] += A[i][j] x[j].
-template <int R, int C>
-__device__ __forceinline__ void dense_add(const double* __restrict__ A, const double (&x)[C],
-                                          double* y) {
+template <int R, int C, typename T>
+__device__ __forceinline__ void dense_add(const T* __restrict__ A, const T (&x)[C], T* y) {
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    double acc = y[i];
+    T acc = y[i];
 #pragma unroll
     for (int j = 0; j < C; ++j) acc = fma(A[i * C + j], x[j], acc);
     y[i] = acc;

@@ -216,6 +216,11 @@ struct dg_mesh_s {
   int64_t launches = 0;
   bool fdm_ok = false;            // FDM tables built (Cartesian meshes)
   double* d_dot = nullptr;        // dot-product scratch: partials + result
+  // fp32 path: rounded Kronecker tables and inverse diagonals
+  KronParamsF kpf{};
+  bool kpf_ok = false;
+  float* d_dinv_gl_f = nullptr;
+  float* d_dinv_pj_f = nullptr;
 };
 
 namespace {
@@ -651,6 +656,8 @@ dg_status dg_mesh_destroy(dg_mesh m) {
   cudaFree(m->d_dinv_gl);
   cudaFree(m->d_dinv_pj);
   cudaFree(m->d_dot);
+  cudaFree(m->d_dinv_gl_f);
+  cudaFree(m->d_dinv_pj_f);
   cudaFree(m->d_recv_lo);
   cudaFree(m->d_recv_hi);
   cudaFree(m->d_send_lo);
@@ -1142,6 +1149,121 @@ dg_status dg_pcg(dg_mesh m, const double* b, double* x, double rel_tol, int32_t 
   }
   if (iters) *iters = k;
   if (rel_res) *rel_res = res;
+  return DG_OK;
+}
+
+}  // extern "C"
+
+// ================================================================ fp32 path (NEXT#3)
+// The Cartesian matvec and the fused Chebyshev smoother in single precision (the paper runs
+// its smoothers and V-cycle in fp32): the same k_kron4
+// kernels instantiated for float, with the 1D tables rounded once from the fp64 setup.
+namespace {
+
+dg_status f32_check(dg_mesh m) {
+  if (!m->cartesian || !kron_v4(m->n))
+    return fail(DG_ERR_UNSUPPORTED, "fp32 path: Cartesian meshes of degree 2..8 on the k_kron4 path only");
+  if (m->zlo == ZSRC_HALO || m->zhi == ZSRC_HALO)
+    return fail(DG_ERR_UNSUPPORTED, "fp32 path: single z-slab only (no fp32 halo buffers)");
+  if (!m->kpf_ok) {
+    const double* src = reinterpret_cast<const double*>(&m->kp);
+    float* dst = reinterpret_cast<float*>(&m->kpf);
+    static_assert(sizeof(KronParams) == 2 * sizeof(KronParamsF), "KronParams layout");
+    for (size_t i = 0; i < sizeof(KronParams) / sizeof(double); ++i) dst[i] = (float)src[i];
+    m->kpf_ok = true;
+  }
+  return DG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dg_status dg_apply_laplace_f32(dg_mesh m, const float* u, float* y, void* stream) {
+  if (!m || !u || !y) return fail(DG_ERR_PARAM, "NULL argument");
+  if (u == y) return fail(DG_ERR_PARAM, "u and y must not alias");
+  dg_status st = f32_check(m);
+  if (st != DG_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  GridArgs g = grid_args(m, 0, m->nz);
+  ChebyArgsF ch{};
+  return post_launch(m, launch_kron4_f32(m->n, m->NL, KMODE_APPLY, m->kpf, g, u, y, ch, s), "kron4_f32", s);
+}
+
+dg_status dg_chebyshev_smooth_f32(dg_mesh m, const float* b, float* x, float* work2, int32_t degree,
+                                  double lambda_max, double lo_frac, double hi_frac, int32_t inner,
+                                  void* stream) {
+  if (!m || !b || !x || !work2) return fail(DG_ERR_PARAM, "NULL argument");
+  if (degree < 0) return fail(DG_ERR_PARAM, "degree < 0");
+  const double alpha = lo_frac * lambda_max, beta = hi_frac * lambda_max;
+  if (!(alpha > 0 && beta > alpha) || !std::isfinite(beta))
+    return fail(DG_ERR_PARAM, "need 0 < lo_frac*lambda_max < hi_frac*lambda_max");
+  if (inner != DG_INNER_GL_JACOBI && inner != DG_INNER_POINT_JACOBI && inner != DG_INNER_FDM)
+    return fail(DG_ERR_PARAM, "bad inner %d", inner);
+  dg_status st = f32_check(m);
+  if (st != DG_OK) return st;
+  if (inner == DG_INNER_FDM && !m->fdm_ok) return fail(DG_ERR_UNSUPPORTED, "FDM tables missing");
+  const int64_t nd = m->ndofs_local;
+  float* W0 = work2;
+  float* W1 = work2 + nd;
+  if ((b >= W0 && b < W1 + nd) || (x >= W0 && x < W1 + nd) || b == x)
+    return fail(DG_ERR_PARAM, "b, x and work2 must not overlap");
+  if (degree == 0) return DG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool fdm = inner == DG_INNER_FDM;
+  const bool gl = inner == DG_INNER_GL_JACOBI && m->desc.basis == DG_BASIS_HERMITE_LIKE;
+  float* dinv = nullptr;
+  if (!fdm) {   // fp32 copy of the fp64 inverse diagonal
+    double** dsrc = gl ? &m->d_dinv_gl : &m->d_dinv_pj;
+    float** fdst = gl ? &m->d_dinv_gl_f : &m->d_dinv_pj_f;
+    if ((st = build_diag(m, inner == DG_INNER_GL_JACOBI, dsrc, s)) != DG_OK) return st;
+    if (!*fdst) {
+      CUDA_TRY(cudaMalloc(fdst, sizeof(float) * (size_t)std::max<int64_t>(nd, 1)));
+      if ((st = post_launch(m, launch_d2f(*dsrc, *fdst, nd, s), "d2f", s)) != DG_OK) return st;
+    }
+    dinv = *fdst;
+  }
+  const int mode = fdm ? KMODE_CHEBY_FDM : (gl ? KMODE_CHEBY_GL : KMODE_CHEBY_PJ);
+  float* buf[3] = {x, W0, W1};
+  std::vector<int> where(degree + 1);
+  where[0] = 0;
+  if (degree == 1) {
+    where[1] = 1;
+  } else if (degree % 2 == 0) {
+    for (int j = 1; j <= degree; ++j) where[j] = (j % 2 == 1) ? 1 : 0;
+  } else {
+    where[1] = 1;
+    where[2] = 2;
+    for (int j = 3; j <= degree; ++j) where[j] = (j % 2 == 1) ? 0 : 2;
+  }
+  const double c = 0.5 * (beta + alpha), delta = 0.5 * (beta - alpha);
+  const double sigma1 = c / delta;
+  double rho = 1.0 / sigma1;
+  GridArgs g = grid_args(m, 0, m->nz);
+  for (int j = 0; j < degree; ++j) {
+    ChebyArgsF ch{};
+    ch.b = b;
+    ch.dinv = dinv;
+    ch.u_next = buf[where[j + 1]];
+    if (j == 0) {
+      ch.first = 1;
+      ch.c_z = 1.0 / c;
+      ch.c_prev = 0.0;
+      ch.u_prev = nullptr;
+    } else {
+      const double rho_n = 1.0 / (2.0 * sigma1 - rho);
+      ch.first = 0;
+      ch.c_prev = rho_n * rho;
+      ch.c_z = 2.0 * rho_n / delta;
+      ch.u_prev = buf[where[j - 1]];
+      rho = rho_n;
+    }
+    st = post_launch(m, launch_kron4_f32(m->n, m->NL, mode, m->kpf, g, buf[where[j]], nullptr, ch, s),
+                     "kron4_f32", s);
+    if (st != DG_OK) return st;
+  }
+  if (where[degree] != 0)
+    CUDA_TRY(cudaMemcpyAsync(x, buf[where[degree]], sizeof(float) * (size_t)nd, cudaMemcpyDeviceToDevice, s));
   return DG_OK;
 }
 

@@ -15,24 +15,27 @@ namespace dgb {
 // Eq. (14)): per direction d, y = sum_d (Mhat (x) Mhat (x) L_d) u + neighbour
 // couplings, L_d = (V/h_d^2) Lhat.  Passed by value (__grid_constant__), so all
 // coefficients live in the constant bank.
-struct KronParams {
-  double M[kEO];               // Mhat, even-odd packed, parity +1
-  double L[3][kEO];            // (V / h_d^2) Lhat, even-odd packed, parity +1
-  double Nm[3][kMaxN * kMaxN]; // [NL][NL]: own rows [0,NL) x neighbour layers [n-NL,n)
-  double Np[3][kMaxN * kMaxN]; // [NL][NL]: own rows [n-NL,n) x neighbour layers [0,NL)
-  double TiT[kEO];             // T^{-T}, even-odd packed
-  double Ti[kEO];              // T^{-1}
+template <typename Real>
+struct KronParamsT {
+  Real M[kEO];               // Mhat, even-odd packed, parity +1
+  Real L[3][kEO];            // (V / h_d^2) Lhat, even-odd packed, parity +1
+  Real Nm[3][kMaxN * kMaxN]; // [NL][NL]: own rows [0,NL) x neighbour layers [n-NL,n)
+  Real Np[3][kMaxN * kMaxN]; // [NL][NL]: own rows [n-NL,n) x neighbour layers [0,NL)
+  Real TiT[kEO];             // T^{-T}, even-odd packed
+  Real Ti[kEO];              // T^{-1}
   // FDM block Jacobi (Eqs. (13)-(15)): L_hat Z = M_hat Z diag(lam), Z^T M_hat Z = I, split by
   // the reflection parity of the eigenvectors (hs symmetric, n - hs antisymmetric ones):
   //   Zs[i*hs + s] = Z[i][sym s]  for rows i < hs (row n/2 is the middle row for odd n)
   //   Za[i*ha + a] = Z[i][anti a] for rows i < n/2
   //   lam[m]: symmetric eigenvalues first, then antisymmetric (the packed eigen index)
   //   cdir[d] = V / h_d^2 (the direction weights of L_d)
-  double Zs[kMaxN * kMaxN];
-  double Za[kMaxN * kMaxN];
-  double lam[kMaxN];
-  double cdir[3];
+  Real Zs[kMaxN * kMaxN];
+  Real Za[kMaxN * kMaxN];
+  Real lam[kMaxN];
+  Real cdir[3];
 };
+using KronParams = KronParamsT<double>;
+using KronParamsF = KronParamsT<float>;   // fp32 path, rounded from KronParams
 
 // Where the z-neighbour layers of the bottom / top local plane come from.
 enum { ZSRC_LOCAL = 0, ZSRC_HALO = 1, ZSRC_MIRROR = 2 };
@@ -49,15 +52,18 @@ struct GridArgs {
 
 enum { KMODE_APPLY = 0, KMODE_CHEBY_GL = 1, KMODE_CHEBY_PJ = 2, KMODE_CHEBY_FDM = 3 };
 
-struct ChebyArgs {
-  const double* b;
-  const double* u_prev;       // may alias u_next (in-place three-term update)
-  double* u_next;
-  const double* dinv;         // inverse diagonal (GL for CHEBY_GL, working basis for CHEBY_PJ)
+template <typename Real>
+struct ChebyArgsT {
+  const Real* b;
+  const Real* u_prev;         // may alias u_next (in-place three-term update)
+  Real* u_next;
+  const Real* dinv;           // inverse diagonal (GL for CHEBY_GL, working basis for CHEBY_PJ)
   double c_prev;              // rho_{j+1} rho_j      (0 on the first step)
   double c_z;                 // 2 rho_{j+1} / delta  (1/c on the first step)
   int first;                  // 1: u_prev is not read
 };
+using ChebyArgs = ChebyArgsT<double>;
+using ChebyArgsF = ChebyArgsT<float>;
 
 struct BchgParams {
   double B[kEO];              // even-odd packed 1D matrix, parity +1
@@ -112,6 +118,8 @@ cudaError_t launch_kron(int n, int NL, int mode, const KronParams& kp, const Gri
 bool kron4_supported(int n);
 cudaError_t launch_kron4(int n, int NL, int mode, const KronParams& kp, const GridArgs& g,
                          const double* u, double* y, const ChebyArgs& ch, cudaStream_t s);
+cudaError_t launch_kron4_f32(int n, int NL, int mode, const KronParamsF& kp, const GridArgs& g,
+                             const float* u, float* y, const ChebyArgsF& ch, cudaStream_t s);
 cudaError_t launch_basis_change(int n, const BchgParams& bp, const double* in, double* out,
                                 int64_t ncells, cudaStream_t s);
 // diagonal of a Cartesian Kronecker operator: d[i,j,k] = sum_d c_d prod(1D diagonals)
@@ -141,6 +149,7 @@ cudaError_t launch_quad3(int n, int NL, int geom, int mode, const QuadParams& qp
 cudaError_t launch_pinv(int n, int inner, const KronParams& kp, const double* r, const double* dinv, double* z,
                         int64_t ncells, cudaStream_t s);
 int dot_partials();
+cudaError_t launch_d2f(const double* in, float* out, int64_t n, cudaStream_t s);
 cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* part, double* out, cudaStream_t s);
 cudaError_t launch_axpby(double alpha, const double* x, double beta, double* y, int64_t n, cudaStream_t s);
 cudaError_t launch_lanczos_start(double* v, int64_t n, int64_t g0, cudaStream_t s);

@@ -7,10 +7,10 @@ namespace dgb {
 
 // FDM transforms (Eqs. (13)-(15)), even/odd by eigenvector parity (see KronParams):
 // forward o = Z^T v (output in the packed eigen index), backward y = Z x.
-template <int N>
-__device__ __forceinline__ void fdm_fwd(const KronParams& kp, const double (&v)[N], double (&o)[N]) {
+template <int N, typename KP, typename T>
+__device__ __forceinline__ void fdm_fwd(const KP& kp, const T (&v)[N], T (&o)[N]) {
   constexpr int H = N / 2, HS = (N + 1) / 2, HA = N / 2;
-  double e[H > 0 ? H : 1], od[H > 0 ? H : 1];
+  T e[H > 0 ? H : 1], od[H > 0 ? H : 1];
 #pragma unroll
   for (int i = 0; i < H; ++i) {
     e[i] = v[i] + v[N - 1 - i];
@@ -18,26 +18,26 @@ __device__ __forceinline__ void fdm_fwd(const KronParams& kp, const double (&v)[
   }
 #pragma unroll
   for (int s = 0; s < HS; ++s) {
-    double acc = (N & 1) ? kp.Zs[H * HS + s] * v[H] : 0.0;
+    T acc = (N & 1) ? kp.Zs[H * HS + s] * v[H] : T(0);
 #pragma unroll
     for (int i = 0; i < H; ++i) acc = fma(kp.Zs[i * HS + s], e[i], acc);
     o[s] = acc;
   }
 #pragma unroll
   for (int a = 0; a < HA; ++a) {
-    double acc = 0.0;
+    T acc = T(0);
 #pragma unroll
     for (int i = 0; i < H; ++i) acc = fma(kp.Za[i * HA + a], od[i], acc);
     o[HS + a] = acc;
   }
 }
 
-template <int N>
-__device__ __forceinline__ void fdm_bwd(const KronParams& kp, const double (&x)[N], double (&y)[N]) {
+template <int N, typename KP, typename T>
+__device__ __forceinline__ void fdm_bwd(const KP& kp, const T (&x)[N], T (&y)[N]) {
   constexpr int H = N / 2, HS = (N + 1) / 2, HA = N / 2;
 #pragma unroll
   for (int i = 0; i < H; ++i) {
-    double E = 0.0, O = 0.0;
+    T E = T(0), O = T(0);
 #pragma unroll
     for (int s = 0; s < HS; ++s) E = fma(kp.Zs[i * HS + s], x[s], E);
 #pragma unroll
@@ -46,7 +46,7 @@ __device__ __forceinline__ void fdm_bwd(const KronParams& kp, const double (&x)[
     y[N - 1 - i] = E - O;
   }
   if (N & 1) {
-    double E = 0.0;
+    T E = T(0);
 #pragma unroll
     for (int s = 0; s < HS; ++s) E = fma(kp.Zs[H * HS + s], x[s], E);
     y[H] = E;

@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "dg_internal.h"
@@ -82,30 +83,31 @@ struct K4Layout {
 
 __device__ __forceinline__ int at(const Lay3& L, int i, int j, int k) { return i + j * L.Pj + k * L.Pk; }
 
-template <int N, int NL, int ALT>
+template <int N, int NL, int ALT, typename Real>
 constexpr int k4_min_blocks() {
   using L = K4Layout<N, NL, ALT>;
-  constexpr int b = (227 * 1024) / L::bytes();
+  constexpr int b = (227 * 1024) / (L::doubles() * (int)sizeof(Real));
   constexpr int t = 2048 / (L::CPB * L::TPC);
   constexpr int m = b < t ? b : t;
-  return m < 1 ? 1 : (m > 3 ? 3 : m);
+  constexpr int cap = sizeof(Real) == 4 ? 5 : 3;
+  return m < 1 ? 1 : (m > cap ? cap : m);
 }
 
 // L2 prefetch of a contiguous range (all threads of the block cooperate, one
 // prefetch per 128-byte line).  Used to pull in the tile one plane up, which a block
 // scheduled about one wave later will read.
-__device__ __forceinline__ void l2_prefetch(const double* p, int64_t ndoubles, int btid, int bt) {
+template <typename T>
+__device__ __forceinline__ void l2_prefetch(const T* p, int64_t count, int btid, int bt) {
   const char* c = reinterpret_cast<const char*>(p);
-  const int64_t bytes = ndoubles * 8;
+  const int64_t bytes = count * (int64_t)sizeof(T);
   for (int64_t o = (int64_t)btid * 128; o < bytes; o += (int64_t)bt * 128)
     asm volatile("prefetch.global.L2 [%0];" ::"l"(c + o));
 }
 
 // M (even-odd) applied to N values read with a stride, written with a stride
-template <int N>
-__device__ __forceinline__ void mass_line(const double* __restrict__ M, const double* src, int ss,
-                                          double* dst, int ds) {
-  double v[N], o[N];
+template <int N, typename T>
+__device__ __forceinline__ void mass_line(const T* __restrict__ M, const T* src, int ss, T* dst, int ds) {
+  T v[N], o[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) v[k] = src[k * ss];
   eo_apply<N, 1>(M, v, o);
@@ -114,23 +116,23 @@ __device__ __forceinline__ void mass_line(const double* __restrict__ M, const do
 }
 
 // P^{-1} building blocks of the fused Chebyshev step: GL-Jacobi (Eq. (12)) or FDM
-template <int N, int MODE>
-__device__ __forceinline__ void pinv_pre(const KronParams& kp, const double (&v)[N], double (&o)[N]) {
+template <int N, int MODE, typename KP, typename T>
+__device__ __forceinline__ void pinv_pre(const KP& kp, const T (&v)[N], T (&o)[N]) {
   if constexpr (MODE == KMODE_CHEBY_FDM) fdm_fwd<N>(kp, v, o);
   else eo_apply<N, 1>(kp.TiT, v, o);
 }
-template <int N, int MODE>
-__device__ __forceinline__ void pinv_post(const KronParams& kp, const double (&v)[N], double (&o)[N]) {
+template <int N, int MODE, typename KP, typename T>
+__device__ __forceinline__ void pinv_post(const KP& kp, const T (&v)[N], T (&o)[N]) {
   if constexpr (MODE == KMODE_CHEBY_FDM) fdm_bwd<N>(kp, v, o);
   else eo_apply<N, 1>(kp.Ti, v, o);
 }
 // middle-stage diagonal of P^{-1} on a line with fixed packed indices (a1, a2) in the
 // other two directions (weights c1, c2) and running index m along direction d (weight cd)
-template <int N, int MODE>
-__device__ __forceinline__ void pinv_diag(const KronParams& kp, const double* __restrict__ dinv, int stride,
-                                          double c1, int a1, double c2, int a2, double cd, double (&o)[N]) {
+template <int N, int MODE, typename KP, typename T>
+__device__ __forceinline__ void pinv_diag(const KP& kp, const T* __restrict__ dinv, int stride, T c1, int a1,
+                                          T c2, int a2, T cd, T (&o)[N]) {
   if constexpr (MODE == KMODE_CHEBY_FDM) {
-    const double base = fma(c1, kp.lam[a1], c2 * kp.lam[a2]);
+    const T base = fma(c1, kp.lam[a1], c2 * kp.lam[a2]);
 #pragma unroll
     for (int m = 0; m < N; ++m) o[m] /= fma(cd, kp.lam[m], base);
   } else {
@@ -139,20 +141,27 @@ __device__ __forceinline__ void pinv_diag(const KronParams& kp, const double* __
   }
 }
 
-template <int N, int NL, int MODE, int OUTD, int ALT>
-__global__ void __launch_bounds__(K4Layout<N, NL, ALT>::CPB * K4Layout<N, NL, ALT>::TPC, (k4_min_blocks<N, NL, ALT>()))
-k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g,
-        const double* __restrict__ u, double* __restrict__ y, const __grid_constant__ ChebyArgs ch) {
+template <typename Real> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+
+template <int N, int NL, int MODE, int OUTD, int ALT, typename Real>
+__global__ void __launch_bounds__(K4Layout<N, NL, ALT>::CPB * K4Layout<N, NL, ALT>::TPC,
+                                  (k4_min_blocks<N, NL, ALT, Real>()))
+k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ GridArgs g,
+        const Real* __restrict__ u, Real* __restrict__ y, const __grid_constant__ ChebyArgsT<Real> ch) {
+  using V2 = typename Vec2<Real>::type;
   using Lay = K4Layout<N, NL, ALT>;
   constexpr int R = Lay::R, NB = Lay::NB, TPC = Lay::TPC, CPB = Lay::CPB;
   constexpr int NN = N * N, N3 = N * NN;
   constexpr Lay3 LZY = Lay::ZY, LYX = Lay::YX, LXZ = Lay::XZ, LOUT = Lay::OUT;
   constexpr int PG = Lay::PG;
-  extern __shared__ double smem[];
-  double* R1 = smem;
-  double* R2 = R1 + CPB * Lay::S1;
-  double* GYb = R2 + CPB * Lay::S2;
-  double* HX = GYb + CPB * Lay::GYC;   // [h][field: 0 = t, 1 = c][l][k][j]
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Real* smem = reinterpret_cast<Real*>(smem_raw);
+  Real* R1 = smem;
+  Real* R2 = R1 + CPB * Lay::S1;
+  Real* GYb = R2 + CPB * Lay::S2;
+  Real* HX = GYb + CPB * Lay::GYC;   // [h][field: 0 = t, 1 = c][l][k][j]
 
   const int ta = threadIdx.x, cslot = threadIdx.y / NB, tb = threadIdx.y - cslot * NB;
   const int cx0 = blockIdx.x * CPB;
@@ -164,9 +173,9 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
   const int64_t plane = (int64_t)g.Nx * g.Ny;
   const int64_t rowcell = ((int64_t)cz * g.Ny + cy) * g.Nx;
   const int64_t cid = rowcell + cx;
-  const double* ucell = u + cid * N3;
+  const Real* ucell = u + cid * N3;
 
-  double* GY = GYb + cslot * Lay::GYC;
+  Real* GY = GYb + cslot * Lay::GYC;
 
   // x-neighbour sources of the block edges (halo cell index or -1)
   const bool xper = g.bc[0] == DG_BC_PERIODIC;
@@ -182,7 +191,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
 
   // z-neighbour sources for this plane
   int zsrc[2];
-  const double* zbase[2];
+  const Real* zbase[2];
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const int nz = cz + (s ? 1 : -1);
@@ -192,9 +201,11 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
     } else {
       zsrc[s] = s ? g.zhi : g.zlo;
       zbase[s] = ucell + (s ? -(int64_t)(g.nz - 1) : (int64_t)(g.nz - 1)) * plane * N3;   // periodic wrap
-      if (zsrc[s] == ZSRC_HALO)
-        zbase[s] = (s ? g.halo_hi : g.halo_lo) + ((int64_t)cy * g.Nx + cx) * (NL * NN) -
-                   (s ? 0 : (N - NL) * NN);
+      if constexpr (std::is_same<Real, double>::value) {   // fp32 meshes are single-slab
+        if (zsrc[s] == ZSRC_HALO)
+          zbase[s] = (s ? g.halo_hi : g.halo_lo) + ((int64_t)cy * g.Nx + cx) * (NL * NN) -
+                     (s ? 0 : (N - NL) * NN);
+      }
     }
   }
 
@@ -209,7 +220,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
   const int nyj = ncell * NYJ;
   const int nh0 = h0 >= 0 ? NL * N : 0, nh1 = h1 >= 0 ? NL * N : 0;
   const int njobs = nyj + nh0 + nh1;
-  auto job_target = [&](int job, const double*& src, double*& dst) {
+  auto job_target = [&](int job, const Real*& src, Real*& dst) {
     if (job < nyj) {
       const int c = job / NYJ, jj = job - c * NYJ;
       const int f = jj / (NL * N), l = (jj / N) % NL, i = jj % N;
@@ -242,9 +253,9 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
     }
   }
   // the first job's loads are issued together with the own z-lines
-  const double* jsrc = nullptr;
-  double* jdst = nullptr;
-  double jv[N];
+  const Real* jsrc = nullptr;
+  Real* jdst = nullptr;
+  Real jv[N];
   if (btid < njobs) job_target(btid, jsrc, jdst);
   if (jsrc) {
 #pragma unroll
@@ -256,24 +267,24 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
       const int zj = tb + r * NB;
       if (N % R != 0 && zj >= N) break;
       const int zi = ta;
-      double uz[N];
+      Real uz[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) uz[k] = __ldg(ucell + k * NN + zj * N + zi);
-      double zm[NL], zp[NL];
+      Real zm[NL], zp[NL];
 #pragma unroll
       for (int l = 0; l < NL; ++l) {
         const int Lm = N - NL + l, Lp = l;
         zm[l] = zsrc[0] == ZSRC_MIRROR ? -uz[N - 1 - Lm] : __ldg(zbase[0] + Lm * NN + zj * N + zi);
         zp[l] = zsrc[1] == ZSRC_MIRROR ? -uz[N - 1 - Lp] : __ldg(zbase[1] + Lp * NN + zj * N + zi);
       }
-      double t[N], a[N];
-      const EOSplit<N> su = eo_split<N>(uz);
+      Real t[N], a[N];
+      const auto su = eo_split<N>(uz);
       eo_mul<N, 1, false>(kp.M, su, t);
       eo_mul<N, 1, false>(kp.L[2], su, a);
       dense_add<NL, NL>(kp.Nm[2], zm, &a[0]);
       dense_add<NL, NL>(kp.Np[2], zp, &a[N - NL]);
-      double* T = R1 + cslot * LZY.CS;
-      double* A = R2 + cslot * LZY.CS;
+      Real* T = R1 + cslot * LZY.CS;
+      Real* A = R2 + cslot * LZY.CS;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         T[at(LZY, zi, zj, k)] = t[k];
@@ -282,15 +293,15 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
     }
   }
   if (jsrc) {
-    double o[N];
+    Real o[N];
     eo_apply<N, 1>(kp.M, jv, o);
 #pragma unroll
     for (int k = 0; k < N; ++k) jdst[k * PG] = o[k];
   }
 #pragma unroll 1
   for (int job = btid + BT; job < njobs; job += BT) {
-    const double* src;
-    double* dst;
+    const Real* src;
+    Real* dst;
     job_target(job, src, dst);
     if (src) mass_line<N>(kp.M, src, NN, dst, PG);
   }
@@ -298,27 +309,27 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
 
   // ================================================================ Y
   {
-    double bl[R][N], cl[R][N];
+    Real bl[R][N], cl[R][N];
     if (active) {
-      const double* T = R1 + cslot * LZY.CS;
-      const double* A = R2 + cslot * LZY.CS;
+      const Real* T = R1 + cslot * LZY.CS;
+      const Real* A = R2 + cslot * LZY.CS;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int yk = tb + r * NB, yi = ta;
         if (N % R != 0 && yk >= N) break;
-        double al[N], tl[N];
+        Real al[N], tl[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) {
           al[j] = A[at(LZY, yi, j, yk)];
           tl[j] = T[at(LZY, yi, j, yk)];
         }
-        double gym[NL], gyp[NL];
+        Real gym[NL], gyp[NL];
 #pragma unroll
         for (int l = 0; l < NL; ++l) {
           gym[l] = ym_row >= 0 ? GY[((0 * NL + l) * N + yk) * PG + yi] : -tl[NL - 1 - l];
           gyp[l] = yp_row >= 0 ? GY[((1 * NL + l) * N + yk) * PG + yi] : -tl[N - 1 - l];
         }
-        const EOSplit<N> st = eo_split<N>(tl);
+        const auto st = eo_split<N>(tl);
         eo_mul2<N, 1>(kp.M, eo_split<N>(al), kp.L[1], st, bl[r]);
         eo_mul<N, 1, false>(kp.M, st, cl[r]);
         dense_add<NL, NL>(kp.Nm[1], gym, &bl[r][0]);
@@ -338,8 +349,8 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
     }
     __syncthreads();   // all of T, A read: their regions take B, C
     if (active) {
-      double* Bf = R1 + cslot * LYX.CS;
-      double* Cf = R2 + cslot * LYX.CS;
+      Real* Bf = R1 + cslot * LYX.CS;
+      Real* Cf = R2 + cslot * LYX.CS;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int yk = tb + r * NB, yi = ta;
@@ -355,10 +366,10 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
   __syncthreads();
 
   // ================================================================ X
-  double res[R][N];
+  Real res[R][N];
   if (active) {
-    const double* Bf = R1 + cslot * LYX.CS;
-    const double* Cf = R2 + cslot * LYX.CS;
+    const Real* Bf = R1 + cslot * LYX.CS;
+    const Real* Cf = R2 + cslot * LYX.CS;
     // x-neighbour c source per side: 1 in-block slot offset, 2 halo, 0 mirror
     const bool inb_m = cslot > 0, inb_p = cslot + 1 < ncell;
     const bool wrap = xper && ncell == g.Nx;   // periodic row inside the block
@@ -369,13 +380,13 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
     for (int r = 0; r < R; ++r) {
       const int xk = tb + r * NB, xj = ta;
       if (N % R != 0 && xk >= N) break;
-      double bl[N], cl[N];
+      Real bl[N], cl[N];
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         bl[i] = Bf[at(LYX, i, xj, xk)];
         cl[i] = Cf[at(LYX, i, xj, xk)];
       }
-      double cxm[NL], cxp[NL];
+      Real cxm[NL], cxp[NL];
 #pragma unroll
       for (int l = 0; l < NL; ++l) {
         const int Lm = N - NL + l, Lp = l;
@@ -397,11 +408,11 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
       for (int r = 0; r < R; ++r) {
         const int xk = tb + r * NB, xj = ta;
         if (N % R != 0 && xk >= N) break;
-        double* out = y + cid * N3 + (xk * N + xj) * N;
+        Real* out = y + cid * N3 + (xk * N + xj) * N;
         if constexpr (N % 2 == 0) {
 #pragma unroll
           for (int i = 0; i < N; i += 2)
-            *reinterpret_cast<double2*>(out + i) = make_double2(res[r][i], res[r][i + 1]);
+            *reinterpret_cast<V2*>(out + i) = V2{res[r][i], res[r][i + 1]};
         } else {
 #pragma unroll
           for (int i = 0; i < N; ++i) out[i] = res[r][i];
@@ -411,7 +422,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
     return;
   } else if constexpr (MODE == KMODE_APPLY) {
     __syncthreads();   // B, C fully read: R1 takes the output
-    double* O = R1 + cslot * LOUT.CS;
+    Real* O = R1 + cslot * LOUT.CS;
     if (active) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -424,7 +435,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
     __syncthreads();
     if (active) {
       // element e = lt + q*TPC of the cell: i = ta, row (j + N k) = tb + q*NB
-      double* out = y + cid * N3;
+      Real* out = y + cid * N3;
 #pragma unroll
       for (int q = 0; q < (NN + NB - 1) / NB; ++q) {
         const int rowi = tb + q * NB;
@@ -439,11 +450,11 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
       for (int r = 0; r < R; ++r) {
         const int xk = tb + r * NB, xj = ta;
         if (N % R != 0 && xk >= N) break;
-        const double* bb = ch.b + cid * N3 + (xk * N + xj) * N;
+        const Real* bb = ch.b + cid * N3 + (xk * N + xj) * N;
         if constexpr (N % 2 == 0) {
 #pragma unroll
           for (int i = 0; i < N; i += 2) {
-            const double2 bv = __ldg(reinterpret_cast<const double2*>(bb + i));
+            const V2 bv = __ldg(reinterpret_cast<const V2*>(bb + i));
             res[r][i] = bv.x - res[r][i];
             res[r][i + 1] = bv.y - res[r][i + 1];
           }
@@ -462,9 +473,9 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         for (int r = 0; r < R; ++r) {
           const int xk = tb + r * NB, xj = ta;
           if (N % R != 0 && xk >= N) break;
-          double o[N];
+          Real o[N];
           pinv_pre<N, MODE>(kp, res[r], o);
-          double* W = R2 + cslot * LYX.CS;
+          Real* W = R2 + cslot * LYX.CS;
 #pragma unroll
           for (int i = 0; i < N; ++i) W[at(LYX, i, xj, xk)] = o[i];
         }
@@ -475,9 +486,9 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         for (int r = 0; r < R; ++r) {
           const int yk = tb + r * NB, yi = ta;
           if (N % R != 0 && yk >= N) break;
-          const double* Rd = R2 + cslot * LYX.CS;
-          double* W = R1 + cslot * LZY.CS;
-          double v[N], o[N];
+          const Real* Rd = R2 + cslot * LYX.CS;
+          Real* W = R1 + cslot * LZY.CS;
+          Real v[N], o[N];
 #pragma unroll
           for (int j = 0; j < N; ++j) v[j] = Rd[at(LYX, yi, j, yk)];
           pinv_pre<N, MODE>(kp, v, o);
@@ -491,9 +502,9 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         for (int r = 0; r < R; ++r) {
           const int zj = tb + r * NB, zi = ta;
           if (N % R != 0 && zj >= N) break;
-          const double* Rd = R1 + cslot * LZY.CS;
-          double* W = R2 + cslot * LZY.CS;
-          double v[N], o[N];
+          const Real* Rd = R1 + cslot * LZY.CS;
+          Real* W = R2 + cslot * LZY.CS;
+          Real v[N], o[N];
 #pragma unroll
           for (int k = 0; k < N; ++k) v[k] = Rd[at(LZY, zi, zj, k)];
           pinv_pre<N, MODE>(kp, v, o);
@@ -510,9 +521,9 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         for (int r = 0; r < R; ++r) {
           const int yk = tb + r * NB, yi = ta;
           if (N % R != 0 && yk >= N) break;
-          const double* Rd = R2 + cslot * LZY.CS;
-          double* W = R1 + cslot * LYX.CS;
-          double v[N], o[N];
+          const Real* Rd = R2 + cslot * LZY.CS;
+          Real* W = R1 + cslot * LYX.CS;
+          Real v[N], o[N];
 #pragma unroll
           for (int j = 0; j < N; ++j) v[j] = Rd[at(LZY, yi, j, yk)];
           pinv_post<N, MODE>(kp, v, o);
@@ -526,39 +537,39 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         for (int r = 0; r < R; ++r) {
           const int xk = tb + r * NB, xj = ta;
           if (N % R != 0 && xk >= N) break;
-          const double* Rd = R1 + cslot * LYX.CS;
-          double v[N], z[N];
+          const Real* Rd = R1 + cslot * LYX.CS;
+          Real v[N], z[N];
 #pragma unroll
           for (int i = 0; i < N; ++i) v[i] = Rd[at(LYX, i, xj, xk)];
           pinv_post<N, MODE>(kp, v, z);
           const int64_t gb = cid * N3 + (xk * N + xj) * N;
 #pragma unroll
           for (int i = 0; i < N; i += 2) {
-            const double2 uj = __ldg(reinterpret_cast<const double2*>(u + gb + i));
-            double2 o;
-            o.x = fma(ch.c_z, z[i], uj.x);
-            o.y = fma(ch.c_z, z[i + 1], uj.y);
+            const V2 uj = __ldg(reinterpret_cast<const V2*>(u + gb + i));
+            V2 o;
+            o.x = fma((Real)ch.c_z, z[i], uj.x);
+            o.y = fma((Real)ch.c_z, z[i + 1], uj.y);
             if (!ch.first) {
-              const double2 up = *reinterpret_cast<const double2*>(ch.u_prev + gb + i);
-              o.x = fma(ch.c_prev, uj.x - up.x, o.x);
-              o.y = fma(ch.c_prev, uj.y - up.y, o.y);
+              const V2 up = *reinterpret_cast<const V2*>(ch.u_prev + gb + i);
+              o.x = fma((Real)ch.c_prev, uj.x - up.x, o.x);
+              o.y = fma((Real)ch.c_prev, uj.y - up.y, o.y);
             }
-            *reinterpret_cast<double2*>(ch.u_next + gb + i) = o;
+            *reinterpret_cast<V2*>(ch.u_next + gb + i) = o;
           }
         }
       }
       return;
     } else if constexpr (MODE == KMODE_CHEBY_GL || MODE == KMODE_CHEBY_FDM) {
-      double* X2 = R2 + cslot * LXZ.CS;
-      double* Z1 = R1 + cslot * LZY.CS;
-      double* Y2 = R2 + cslot * LYX.CS;
-      double* X1 = R1 + cslot * LXZ.CS;
+      Real* X2 = R2 + cslot * LXZ.CS;
+      Real* Z1 = R1 + cslot * LZY.CS;
+      Real* Y2 = R2 + cslot * LYX.CS;
+      Real* X1 = R1 + cslot * LXZ.CS;
       if (active) {   // x: T^{-T}
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int xk = tb + r * NB, xj = ta;
           if (N % R != 0 && xk >= N) break;
-          double o[N];
+          Real o[N];
           pinv_pre<N, MODE>(kp, res[r], o);
 #pragma unroll
           for (int i = 0; i < N; ++i) X2[at(LXZ, i, xj, xk)] = o[i];
@@ -570,7 +581,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         for (int r = 0; r < R; ++r) {
           const int zj = tb + r * NB, zi = ta;
           if (N % R != 0 && zj >= N) break;
-          double v[N], o[N];
+          Real v[N], o[N];
 #pragma unroll
           for (int k = 0; k < N; ++k) v[k] = X2[at(LXZ, zi, zj, k)];
           pinv_pre<N, MODE>(kp, v, o);
@@ -584,7 +595,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         for (int r = 0; r < R; ++r) {
           const int yk = tb + r * NB, yi = ta;
           if (N % R != 0 && yk >= N) break;
-          double v[N], o[N];
+          Real v[N], o[N];
 #pragma unroll
           for (int j = 0; j < N; ++j) v[j] = Z1[at(LZY, yi, j, yk)];
           pinv_pre<N, MODE>(kp, v, o);
@@ -601,7 +612,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         for (int r = 0; r < R; ++r) {
           const int xk = tb + r * NB, xj = ta;
           if (N % R != 0 && xk >= N) break;
-          double v[N], o[N];
+          Real v[N], o[N];
 #pragma unroll
           for (int i = 0; i < N; ++i) v[i] = Y2[at(LYX, i, xj, xk)];
           pinv_post<N, MODE>(kp, v, o);
@@ -615,7 +626,7 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
         for (int r = 0; r < R; ++r) {
           const int zj = tb + r * NB, zi = ta;
           if (N % R != 0 && zj >= N) break;
-          double v[N];
+          Real v[N];
 #pragma unroll
           for (int k = 0; k < N; ++k) v[k] = X1[at(LXZ, zi, zj, k)];
           pinv_post<N, MODE>(kp, v, res[r]);
@@ -623,13 +634,13 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
       }
     } else {
       // point Jacobi: diagonal along the x-lines, then to z-lines through smem
-      double* X1 = R1 + cslot * LXZ.CS;
+      Real* X1 = R1 + cslot * LXZ.CS;
       if (active) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int xk = tb + r * NB, xj = ta;
           if (N % R != 0 && xk >= N) break;
-          const double* dv = ch.dinv + cid * N3 + (xk * N + xj) * N;
+          const Real* dv = ch.dinv + cid * N3 + (xk * N + xj) * N;
 #pragma unroll
           for (int i = 0; i < N; ++i) X1[at(LXZ, i, xj, xk)] = res[r][i] * __ldg(dv + i);
         }
@@ -655,9 +666,9 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
 #pragma unroll
         for (int k = 0; k < N; ++k) {
           const int64_t gi = gbase + k * NN;
-          const double uj = __ldg(u + gi);   // re-read (L1/L2): saves R*N live registers
-          double v = fma(ch.c_z, res[r][k], uj);
-          if (!ch.first) v = fma(ch.c_prev, uj - ch.u_prev[gi], v);
+          const Real uj = __ldg(u + gi);   // re-read (L1/L2): saves R*N live registers
+          Real v = fma((Real)ch.c_z, res[r][k], uj);
+          if (!ch.first) v = fma((Real)ch.c_prev, uj - ch.u_prev[gi], v);
           ch.u_next[gi] = v;
         }
       }
@@ -665,26 +676,26 @@ k_kron4(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
   }
 }
 
-template <int N, int NL, int MODE, int OUTD, int ALT>
-cudaError_t launch_t(const KronParams& kp, const GridArgs& g, const double* u, double* y,
-                     const ChebyArgs& ch, cudaStream_t s) {
+template <int N, int NL, int MODE, int OUTD, int ALT, typename Real>
+cudaError_t launch_t(const KronParamsT<Real>& kp, const GridArgs& g, const Real* u, Real* y,
+                     const ChebyArgsT<Real>& ch, cudaStream_t s) {
   using Lay = K4Layout<N, NL, ALT>;
   const int planes = g.zend - g.zbeg;
   if (planes <= 0 || g.Nx <= 0 || g.Ny <= 0) return cudaSuccess;
   if (g.Ny > 65535 || planes > 65535) return cudaErrorInvalidValue;
   const dim3 grid((g.Nx + Lay::CPB - 1) / Lay::CPB, g.Ny, planes);
   const dim3 block(N, Lay::NB * Lay::CPB);
-  const size_t smem = Lay::bytes();
-  auto kern = k_kron4<N, NL, MODE, OUTD, ALT>;
+  const size_t smem = (size_t)Lay::doubles() * sizeof(Real);
+  auto kern = k_kron4<N, NL, MODE, OUTD, ALT, Real>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, block, smem, s>>>(kp, g, u, y, ch);
   return cudaGetLastError();
 }
 
-template <int N, int NL>
-cudaError_t launch_mode(int mode, const KronParams& kp, const GridArgs& g, const double* u,
-                        double* y, const ChebyArgs& ch, cudaStream_t s) {
+template <int N, int NL, typename Real>
+cudaError_t launch_mode(int mode, const KronParamsT<Real>& kp, const GridArgs& g, const Real* u, Real* y,
+                        const ChebyArgsT<Real>& ch, cudaStream_t s) {
   static const int outd = [] {   // DG_K4_OUT=0: smem-staged coalesced stores (comparison)
     const char* e = std::getenv("DG_K4_OUT");
     return e ? std::atoi(e) : (N % 2 == 0 ? 1 : 0);   // measured: direct wins for even n only
@@ -697,31 +708,31 @@ cudaError_t launch_mode(int mode, const KronParams& kp, const GridArgs& g, const
     if (alt == 1) {
       switch (mode) {
         case KMODE_APPLY:
-          return outd ? launch_t<N, NL, KMODE_APPLY, 1, 1>(kp, g, u, y, ch, s)
-                      : launch_t<N, NL, KMODE_APPLY, 0, 1>(kp, g, u, y, ch, s);
-        case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 1>(kp, g, u, y, ch, s);
-        case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 1>(kp, g, u, y, ch, s);
-        case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 1>(kp, g, u, y, ch, s);
+          return outd ? launch_t<N, NL, KMODE_APPLY, 1, 1, Real>(kp, g, u, y, ch, s)
+                      : launch_t<N, NL, KMODE_APPLY, 0, 1, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 1, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 1, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 1, Real>(kp, g, u, y, ch, s);
       }
       return cudaErrorInvalidValue;
     }
   }
   switch (mode) {
     case KMODE_APPLY:
-      return outd ? launch_t<N, NL, KMODE_APPLY, 1, 0>(kp, g, u, y, ch, s)
-                  : launch_t<N, NL, KMODE_APPLY, 0, 0>(kp, g, u, y, ch, s);
-    case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 0>(kp, g, u, y, ch, s);
-    case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 0>(kp, g, u, y, ch, s);
-    case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 0>(kp, g, u, y, ch, s);
+      return outd ? launch_t<N, NL, KMODE_APPLY, 1, 0, Real>(kp, g, u, y, ch, s)
+                  : launch_t<N, NL, KMODE_APPLY, 0, 0, Real>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 0, Real>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 0, Real>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 0, Real>(kp, g, u, y, ch, s);
   }
   return cudaErrorInvalidValue;
 }
 
-template <int N>
-cudaError_t launch_nl(int NL, int mode, const KronParams& kp, const GridArgs& g, const double* u,
-                      double* y, const ChebyArgs& ch, cudaStream_t s) {
-  if (NL == 2 && N > 2) return launch_mode<N, 2>(mode, kp, g, u, y, ch, s);
-  if (NL == N) return launch_mode<N, N>(mode, kp, g, u, y, ch, s);
+template <int N, typename Real>
+cudaError_t launch_nl(int NL, int mode, const KronParamsT<Real>& kp, const GridArgs& g, const Real* u, Real* y,
+                      const ChebyArgsT<Real>& ch, cudaStream_t s) {
+  if (NL == 2 && N > 2) return launch_mode<N, 2, Real>(mode, kp, g, u, y, ch, s);
+  if (NL == N) return launch_mode<N, N, Real>(mode, kp, g, u, y, ch, s);
   return cudaErrorInvalidValue;
 }
 
@@ -730,18 +741,29 @@ cudaError_t launch_nl(int NL, int mode, const KronParams& kp, const GridArgs& g,
 // n in 3..9 (p = 2..8); other degrees use k_kron.cu
 bool kron4_supported(int n) { return n >= 3 && n <= 9; }
 
-cudaError_t launch_kron4(int n, int NL, int mode, const KronParams& kp, const GridArgs& g,
-                         const double* u, double* y, const ChebyArgs& ch, cudaStream_t s) {
+template <typename Real>
+cudaError_t launch_kron4_t(int n, int NL, int mode, const KronParamsT<Real>& kp, const GridArgs& g, const Real* u,
+                           Real* y, const ChebyArgsT<Real>& ch, cudaStream_t s) {
   switch (n) {
-    case 3: return launch_nl<3>(NL, mode, kp, g, u, y, ch, s);
-    case 4: return launch_nl<4>(NL, mode, kp, g, u, y, ch, s);
-    case 5: return launch_nl<5>(NL, mode, kp, g, u, y, ch, s);
-    case 6: return launch_nl<6>(NL, mode, kp, g, u, y, ch, s);
-    case 7: return launch_nl<7>(NL, mode, kp, g, u, y, ch, s);
-    case 8: return launch_nl<8>(NL, mode, kp, g, u, y, ch, s);
-    case 9: return launch_nl<9>(NL, mode, kp, g, u, y, ch, s);
+    case 3: return launch_nl<3, Real>(NL, mode, kp, g, u, y, ch, s);
+    case 4: return launch_nl<4, Real>(NL, mode, kp, g, u, y, ch, s);
+    case 5: return launch_nl<5, Real>(NL, mode, kp, g, u, y, ch, s);
+    case 6: return launch_nl<6, Real>(NL, mode, kp, g, u, y, ch, s);
+    case 7: return launch_nl<7, Real>(NL, mode, kp, g, u, y, ch, s);
+    case 8: return launch_nl<8, Real>(NL, mode, kp, g, u, y, ch, s);
+    case 9: return launch_nl<9, Real>(NL, mode, kp, g, u, y, ch, s);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_kron4(int n, int NL, int mode, const KronParams& kp, const GridArgs& g,
+                         const double* u, double* y, const ChebyArgs& ch, cudaStream_t s) {
+  return launch_kron4_t<double>(n, NL, mode, kp, g, u, y, ch, s);
+}
+
+cudaError_t launch_kron4_f32(int n, int NL, int mode, const KronParamsF& kp, const GridArgs& g,
+                             const float* u, float* y, const ChebyArgsF& ch, cudaStream_t s) {
+  return launch_kron4_t<float>(n, NL, mode, kp, g, u, y, ch, s);
 }
 
 }  // namespace dgb

@@ -145,6 +145,11 @@ __global__ void k_lanczos_start(double* __restrict__ v, int64_t n, int64_t g0) {
     v[i] = (double)((g0 + i) % 12) - 5.5;
 }
 
+__global__ void k_d2f(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)in[i];
+}
+
 template <int N, int INNER>
 cudaError_t launch_pinv_n(const KronParams& kp, const double* r, const double* dinv, double* z, int64_t ncells,
                           cudaStream_t s) {
@@ -185,6 +190,12 @@ cudaError_t launch_pinv(int n, int inner, const KronParams& kp, const double* r,
 }
 
 int dot_partials() { return kDotBlocks; }
+
+cudaError_t launch_d2f(const double* in, float* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_d2f<<<148 * 8, 256, 0, s>>>(in, out, n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* part, double* out, cudaStream_t s) {
   k_dot1<<<kDotBlocks, kDotThreads, 0, s>>>(a, b, n, part);

@@ -356,3 +356,56 @@ def test_gpu_pcg_solves():
     it, res = m.pcg(_dev(b), x, lmax, rel_tol=1e-11, max_iter=200, cheby_degree=3)
     assert res <= 1e-11 and it < 60
     assert _rel(x.cpu().numpy(), xs) <= 1e-9
+
+
+# ---------------------------------------------------------------- fp32 path (NEXT#3)
+# Tolerance: inputs are rounded to float once and the oracle is applied to
+# the rounded input in fp64, so the difference is the fp32 arithmetic alone: ~50 rounded
+# operations per output (7 even-odd sweeps + couplings) at unit roundoff 6e-8, amplified by
+# the cancellation of the Laplacian of a random vector (|A||u| / |Au| ~ 3-10): <= 1e-5.
+TOL32 = 1e-5
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 6, 7, 8])
+def test_matvec_f32(p):
+    _needs_gpu()
+    spec = MeshSpec(degree=p, n_cells=(3, 2, 4), box_hi=(1.0, 0.8, 1.3),
+                    bc=("dirichlet", "periodic", "dirichlet"), seed=110 + p)
+    u32 = uniform_vector(spec.n_dofs, spec.seed).astype(np.float32)
+    ref = _oracle(spec).apply(u32.astype(np.float64))
+    m = _gpu_mesh(spec)
+    y = m.apply_laplace_f32(torch.from_numpy(u32).cuda()).cpu().numpy().astype(np.float64)
+    assert _rel(y, ref) <= TOL32
+
+
+@pytest.mark.parametrize("p", [3, 5, 8])
+@pytest.mark.parametrize("inner", ["gl_jacobi", "fdm", "point_jacobi"])
+def test_chebyshev_f32(p, inner):
+    _needs_gpu()
+    from oracle import fdm
+    from oracle import smoother as sm
+    from oracle.geometry import mesh_from_spec
+    from oracle.sipg import SIPG
+    spec = MeshSpec(degree=p, n_cells=(3, 2, 4), box_hi=(1.0, 0.8, 1.3),
+                    bc=("dirichlet", "periodic", "dirichlet"), seed=120 + p)
+    om = mesh_from_spec(spec)
+    H = SIPG(om, p)
+    P = {"gl_jacobi": lambda: sm.GLJacobi(SIPG(om, p, "gl")), "point_jacobi": lambda: sm.PointJacobi(H),
+         "fdm": lambda: fdm.FDM(p, (1.0 / 3, 0.8 / 2, 1.3 / 4))}[inner]()
+    b32 = uniform_vector(spec.n_dofs, 130 + p).astype(np.float32)
+    x32 = uniform_vector(spec.n_dofs, 140 + p).astype(np.float32)
+    lmax = 2.0
+    ref = sm.chebyshev(H.apply, P, b32.astype(np.float64), x32.astype(np.float64), 3, lmax)
+    m = _gpu_mesh(spec)
+    x = torch.from_numpy(x32).cuda()
+    m.chebyshev_smooth_f32(torch.from_numpy(b32).cuda(), x, lmax, degree=3, inner=inner)
+    assert _rel(x.cpu().numpy().astype(np.float64), ref) <= TOL32
+
+
+def test_f32_unsupported_on_curved_mesh():
+    _needs_gpu()
+    spec = MeshSpec(degree=3, n_cells=(2, 2, 2), deform_amp=0.05, geometry="per_qpoint", seed=1)
+    m = _gpu_mesh(spec)
+    u = torch.zeros(spec.n_dofs, dtype=torch.float32, device="cuda")
+    with pytest.raises(Exception, match="fp32"):
+        m.apply_laplace_f32(u)
