@@ -363,7 +363,7 @@ def test_gpu_pcg_solves():
 # the rounded input in fp64, so the difference is the fp32 arithmetic alone: ~50 rounded
 # operations per output (7 even-odd sweeps + couplings) at unit roundoff 6e-8, amplified by
 # the cancellation of the Laplacian of a random vector (|A||u| / |Au| ~ 3-10): <= 1e-5.
-TOL32 = 1e-5
+TOL32 = 2e-6   # bound 1e-5 (above); measured <= 1.9e-7 (profiles/r1_f32_errors.txt)
 
 
 @pytest.mark.parametrize("p", [2, 3, 4, 5, 6, 7, 8])
