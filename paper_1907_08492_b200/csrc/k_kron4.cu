@@ -63,8 +63,10 @@ template <int N> struct K4HasAlt { static constexpr bool value = N == 6 || N == 
 
 constexpr int imax(int a, int b) { return a > b ? a : b; }
 
-template <int N, int NL, int ALT = 0>
+template <int N, int NL, int ALT = 0, int MODE = KMODE_APPLY>
 struct K4Layout {
+  // the x->z layout is only used by point Jacobi and by the odd-n Chebyshev order
+  static constexpr bool USE_XZ = MODE == KMODE_CHEBY_PJ || (N % 2 == 1 && MODE != KMODE_APPLY);
   static constexpr int R = K4C<N, ALT>::R, CPB = K4C<N, ALT>::CPB;
   static constexpr int NB = (N + R - 1) / R;          // thread rows per cell
   static constexpr int TPC = N * NB;                   // threads per cell
@@ -72,8 +74,8 @@ struct K4Layout {
   static constexpr int P = N | 1;                      // output staging row pitch
   static constexpr Lay3 OUT{P, N * P, N * N * P};
   // R1: T -> B -> (P^-1: z->y, x->z) -> output;  R2: A -> C -> (P^-1: x->z, y->x)
-  static constexpr int S1 = imax(imax(imax(ZY.CS, YX.CS), OUT.CS), XZ.CS);
-  static constexpr int S2 = imax(imax(ZY.CS, YX.CS), XZ.CS);
+  static constexpr int S1 = imax(imax(imax(ZY.CS, YX.CS), OUT.CS), USE_XZ ? XZ.CS : 0);
+  static constexpr int S2 = imax(imax(ZY.CS, YX.CS), USE_XZ ? XZ.CS : 0);
   static constexpr int PG = N | 1;
   static constexpr int GYC = 2 * NL * N * PG;          // y-ghost rows per cell [f][l][k][i]
   static constexpr int HS = NL * N * PG;               // one x-halo field [l][k][j]
@@ -83,13 +85,13 @@ struct K4Layout {
 
 __device__ __forceinline__ int at(const Lay3& L, int i, int j, int k) { return i + j * L.Pj + k * L.Pk; }
 
-template <int N, int NL, int ALT, typename Real>
+template <int N, int NL, int ALT, typename Real, int MODE>
 constexpr int k4_min_blocks() {
-  using L = K4Layout<N, NL, ALT>;
+  using L = K4Layout<N, NL, ALT, MODE>;
   constexpr int b = (227 * 1024) / (L::doubles() * (int)sizeof(Real));
   constexpr int t = 2048 / (L::CPB * L::TPC);
   constexpr int m = b < t ? b : t;
-  constexpr int cap = sizeof(Real) == 4 ? 5 : 3;
+  constexpr int cap = sizeof(Real) == 4 ? (N == 7 ? 3 : 5) : (N == 3 ? 4 : 3);   // measured (r1)
   return m < 1 ? 1 : (m > cap ? cap : m);
 }
 
@@ -147,11 +149,11 @@ template <> struct Vec2<float> { using type = float2; };
 
 template <int N, int NL, int MODE, int OUTD, int ALT, typename Real>
 __global__ void __launch_bounds__(K4Layout<N, NL, ALT>::CPB * K4Layout<N, NL, ALT>::TPC,
-                                  (k4_min_blocks<N, NL, ALT, Real>()))
+                                  (k4_min_blocks<N, NL, ALT, Real, MODE>()))
 k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ GridArgs g,
         const Real* __restrict__ u, Real* __restrict__ y, const __grid_constant__ ChebyArgsT<Real> ch) {
   using V2 = typename Vec2<Real>::type;
-  using Lay = K4Layout<N, NL, ALT>;
+  using Lay = K4Layout<N, NL, ALT, MODE>;
   constexpr int R = Lay::R, NB = Lay::NB, TPC = Lay::TPC, CPB = Lay::CPB;
   constexpr int NN = N * N, N3 = N * NN;
   constexpr Lay3 LZY = Lay::ZY, LYX = Lay::YX, LXZ = Lay::XZ, LOUT = Lay::OUT;
@@ -679,7 +681,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
 template <int N, int NL, int MODE, int OUTD, int ALT, typename Real>
 cudaError_t launch_t(const KronParamsT<Real>& kp, const GridArgs& g, const Real* u, Real* y,
                      const ChebyArgsT<Real>& ch, cudaStream_t s) {
-  using Lay = K4Layout<N, NL, ALT>;
+  using Lay = K4Layout<N, NL, ALT, MODE>;
   const int planes = g.zend - g.zbeg;
   if (planes <= 0 || g.Nx <= 0 || g.Ny <= 0) return cudaSuccess;
   if (g.Ny > 65535 || planes > 65535) return cudaErrorInvalidValue;
