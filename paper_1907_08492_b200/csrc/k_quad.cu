@@ -634,28 +634,52 @@ __global__ void k_diag_general(const __grid_constant__ DiagTables t, const __gri
     for (int f = 0; f < 6; ++f) {
       const int d = f >> 1, s = f & 1;
       const double v = t.v[s][ii[d]], dv = t.d[s][ii[d]];
-      if (v == 0.0 && dv == 0.0) continue;
       const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
       const int cd = d == 0 ? cx : (d == 1 ? cy : czl);
       const int Nd = d == 0 ? g.Nx : (d == 1 ? g.Ny : g.nz);
       const int nb = cd + (s ? 1 : -1);
-      bool mirror = false;
+      bool mirror = false, self = false;
       if (nb < 0 || nb >= Nd) {
         if (d < 2) mirror = g.bc[d] != DG_BC_PERIODIC;
         else mirror = (s == 0 ? g.zlo : g.zhi) == ZSRC_MIRROR;
+        // periodic with one cell in this direction: the neighbour is the cell itself, so
+        // the trial function l_i is also nonzero on the other side of the face
+        self = !mirror && Nd == 1 && (d < 2 || (s == 0 ? g.zlo : g.zhi) == ZSRC_LOCAL);
       }
-      const double mf = mirror ? 2.0 : 1.0;
+      const double vp = self ? t.v[1 - s][ii[d]] : 0.0, dvp = self ? t.d[1 - s][ii[d]] : 0.0;
+      if (v == 0.0 && dv == 0.0 && vp == 0.0 && dvp == 0.0) continue;
       for (int qb = 0; qb < N; ++qb)
         for (int qa = 0; qa < N; ++qa) {
           double ckm[3], ckp[3], sdA;
           face_geom<N, GEOM>(qp, ga, g, cid, cx, cy, czl, f, qa, qb, ckm, ckp, sdA, mirror);
           const double sa = t.S[qa * N + ii[t1]], sb = t.S[qb * N + ii[t2]];
+          const double da = t.DS[qa * N + ii[t1]], db = t.DS[qb * N + ii[t2]];
+          // own side (test and trial): value and reference gradient of l_i at the face point
           const double l = v * sa * sb;
           double gr[3];
           gr[d] = dv * sa * sb;
-          gr[t1] = v * t.DS[qa * N + ii[t1]] * sb;
-          gr[t2] = v * sa * t.DS[qb * N + ii[t2]];
-          acc += mf * (sdA * l * l - l * (ckm[0] * gr[0] + ckm[1] * gr[1] + ckm[2] * gr[2]));
+          gr[t1] = v * da * sb;
+          gr[t2] = v * sa * db;
+          const double cg = ckm[0] * gr[0] + ckm[1] * gr[1] + ckm[2] * gr[2];
+          // other side of the face (Eq. (1)): 0 (interior: l_i lives on K only), the mirror
+          // ghost (-l, grad l), or l_i itself at the opposite face (self-periodic)
+          double up, cgp;
+          if (mirror) {
+            up = -l;
+            cgp = cg;
+          } else if (self) {
+            up = vp * sa * sb;
+            double grp[3];
+            grp[d] = dvp * sa * sb;
+            grp[t1] = vp * da * sb;
+            grp[t2] = vp * sa * db;
+            cgp = ckp[0] * grp[0] + ckp[1] * grp[1] + ckp[2] * grp[2];
+          } else {
+            up = 0.0;
+            cgp = 0.0;
+          }
+          const double jump = l - up;
+          acc += sdA * jump * l - 0.5 * l * (cg + cgp) - 0.5 * cg * jump;
         }
     }
     out[gi] = invert ? 1.0 / acc : acc;

@@ -409,3 +409,29 @@ def test_f32_unsupported_on_curved_mesh():
     u = torch.zeros(spec.n_dofs, dtype=torch.float32, device="cuda")
     with pytest.raises(Exception, match="fp32"):
         m.apply_laplace_f32(u)
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+@pytest.mark.parametrize("nc,bcx", [((11, 2, 2), "periodic"), ((13, 2, 3), "dirichlet"), ((33, 1, 2), "periodic")])
+def test_rows_longer_than_a_block(p, nc, bcx):
+    """Row-aligned blocks (k_kron4 / k_quad3): rows of several blocks with a ragged last
+    block, the x-neighbours of the block-edge cells from halo jobs (periodic wrap across
+    blocks), for the Cartesian and the curved per-q-point paths and the Chebyshev step."""
+    _needs_gpu()
+    from oracle import smoother as sm
+    from oracle.geometry import mesh_from_spec
+    from oracle.sipg import SIPG
+    for geom, amp in (("constant", 0.0), ("per_qpoint", 0.03)):
+        spec = MeshSpec(degree=p, n_cells=nc, bc=(bcx, "periodic", "dirichlet"), geometry=geom,
+                        deform_amp=amp, seed=150 + p)
+        u = uniform_vector(spec.n_dofs, spec.seed)
+        om = mesh_from_spec(spec)
+        H = SIPG(om, p)
+        m = _gpu_mesh(spec)
+        assert _rel(m.apply_laplace(_dev(u)).cpu().numpy(), H.apply(u)) <= TOL, geom
+        if p in (3, 5):
+            b = uniform_vector(spec.n_dofs, 160 + p)
+            ref = sm.chebyshev(H.apply, sm.GLJacobi(SIPG(om, p, "gl")), b, u, 2, 2.4)
+            x = _dev(u)
+            m.chebyshev_smooth(_dev(b), x, 2.4, degree=2)
+            assert _rel(x.cpu().numpy(), ref) <= TOL, geom
