@@ -429,6 +429,10 @@ def test_rows_longer_than_a_block(p, nc, bcx):
         H = SIPG(om, p)
         m = _gpu_mesh(spec)
         assert _rel(m.apply_laplace(_dev(u)).cpu().numpy(), H.apply(u)) <= TOL, geom
+        if geom == "constant":   # fp32 path on the same block structure
+            u32 = u.astype(np.float32)
+            y32 = m.apply_laplace_f32(torch.from_numpy(u32).cuda()).cpu().numpy().astype(np.float64)
+            assert _rel(y32, H.apply(u32.astype(np.float64))) <= TOL32
         if p in (3, 5):
             b = uniform_vector(spec.n_dofs, 160 + p)
             ref = sm.chebyshev(H.apply, sm.GLJacobi(SIPG(om, p, "gl")), b, u, 2, 2.4)
