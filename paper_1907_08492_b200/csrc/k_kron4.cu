@@ -369,6 +369,21 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
 
   // ================================================================ X
   Real res[R][N];
+  // Chebyshev, even n: issue the x-line loads of b before the stage's arithmetic
+  constexpr bool kPreB = MODE != KMODE_APPLY && N % 2 == 0;
+  V2 bpre[kPreB ? R : 1][kPreB ? N / 2 : 1];
+  if constexpr (kPreB) {
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int xk = tb + r * NB, xj = ta;
+        if (N % R != 0 && xk >= N) break;
+        const Real* bb = ch.b + cid * N3 + (xk * N + xj) * N;
+#pragma unroll
+        for (int i = 0; i < N; i += 2) bpre[r][i / 2] = __ldg(reinterpret_cast<const V2*>(bb + i));
+      }
+    }
+  }
   if (active) {
     const Real* Bf = R1 + cslot * LYX.CS;
     const Real* Cf = R2 + cslot * LYX.CS;
@@ -453,10 +468,10 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
         const int xk = tb + r * NB, xj = ta;
         if (N % R != 0 && xk >= N) break;
         const Real* bb = ch.b + cid * N3 + (xk * N + xj) * N;
-        if constexpr (N % 2 == 0) {
+        if constexpr (kPreB) {
 #pragma unroll
           for (int i = 0; i < N; i += 2) {
-            const V2 bv = __ldg(reinterpret_cast<const V2*>(bb + i));
+            const V2 bv = bpre[r][i / 2];
             res[r][i] = bv.x - res[r][i];
             res[r][i + 1] = bv.y - res[r][i + 1];
           }
@@ -483,6 +498,19 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
         }
       }
       __syncthreads();
+      Real dpre[MODE == KMODE_CHEBY_GL ? R : 1][MODE == KMODE_CHEBY_GL ? N : 1];
+      if constexpr (MODE == KMODE_CHEBY_GL) {   // the next stage's diagonal, loaded one stage early
+        if (active) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int zj = tb + r * NB, zi = ta;
+            if (N % R != 0 && zj >= N) break;
+            const Real* dv = ch.dinv + cid * N3 + zj * N + zi;
+#pragma unroll
+            for (int k = 0; k < N; ++k) dpre[r][k] = __ldg(dv + k * NN);
+          }
+        }
+      }
       if (active) {   // y: T^{-T} -> R1 (y-write / z-read)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -510,14 +538,33 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
 #pragma unroll
           for (int k = 0; k < N; ++k) v[k] = Rd[at(LZY, zi, zj, k)];
           pinv_pre<N, MODE>(kp, v, o);
-          pinv_diag<N, MODE>(kp, ch.dinv + cid * N3 + zj * N + zi, NN, kp.cdir[0], zi, kp.cdir[1], zj,
-                             kp.cdir[2], o);
+          if constexpr (MODE == KMODE_CHEBY_GL) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) o[k] *= dpre[r][k];
+          } else {
+            pinv_diag<N, MODE>(kp, ch.dinv + cid * N3 + zj * N + zi, NN, kp.cdir[0], zi, kp.cdir[1], zj,
+                               kp.cdir[2], o);
+          }
           pinv_post<N, MODE>(kp, o, v);
 #pragma unroll
           for (int k = 0; k < N; ++k) W[at(LZY, zi, zj, k)] = v[k];
         }
       }
       __syncthreads();
+      V2 ujpre[R][N / 2], uppre[R][N / 2];   // the update's inputs, loaded one stage early
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int xk = tb + r * NB, xj = ta;
+          if (N % R != 0 && xk >= N) break;
+          const int64_t gb = cid * N3 + (xk * N + xj) * N;
+#pragma unroll
+          for (int i = 0; i < N; i += 2) {
+            ujpre[r][i / 2] = __ldg(reinterpret_cast<const V2*>(u + gb + i));
+            if (!ch.first) uppre[r][i / 2] = *reinterpret_cast<const V2*>(ch.u_prev + gb + i);
+          }
+        }
+      }
       if (active) {   // y: T^{-1} -> R1 (y-write / x-read)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -547,12 +594,12 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
           const int64_t gb = cid * N3 + (xk * N + xj) * N;
 #pragma unroll
           for (int i = 0; i < N; i += 2) {
-            const V2 uj = __ldg(reinterpret_cast<const V2*>(u + gb + i));
+            const V2 uj = ujpre[r][i / 2];
             V2 o;
             o.x = fma((Real)ch.c_z, z[i], uj.x);
             o.y = fma((Real)ch.c_z, z[i + 1], uj.y);
             if (!ch.first) {
-              const V2 up = *reinterpret_cast<const V2*>(ch.u_prev + gb + i);
+              const V2 up = uppre[r][i / 2];
               o.x = fma((Real)ch.c_prev, uj.x - up.x, o.x);
               o.y = fma((Real)ch.c_prev, uj.y - up.y, o.y);
             }
