@@ -625,6 +625,19 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
         }
       }
       __syncthreads();
+      Real dpre[MODE == KMODE_CHEBY_GL ? R : 1][MODE == KMODE_CHEBY_GL ? N : 1];
+      if constexpr (MODE == KMODE_CHEBY_GL) {   // the y stage's diagonal, loaded one stage early
+        if (active) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int yk = tb + r * NB, yi = ta;
+            if (N % R != 0 && yk >= N) break;
+            const Real* dv = ch.dinv + cid * N3 + yk * NN + yi;
+#pragma unroll
+            for (int j = 0; j < N; ++j) dpre[r][j] = __ldg(dv + j * N);
+          }
+        }
+      }
       if (active) {   // z: T^{-T}
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -648,14 +661,33 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
 #pragma unroll
           for (int j = 0; j < N; ++j) v[j] = Z1[at(LZY, yi, j, yk)];
           pinv_pre<N, MODE>(kp, v, o);
-          pinv_diag<N, MODE>(kp, ch.dinv + cid * N3 + yk * NN + yi, N, kp.cdir[0], yi, kp.cdir[2], yk,
-                             kp.cdir[1], o);
+          if constexpr (MODE == KMODE_CHEBY_GL) {
+#pragma unroll
+            for (int j = 0; j < N; ++j) o[j] *= dpre[r][j];
+          } else {
+            pinv_diag<N, MODE>(kp, ch.dinv + cid * N3 + yk * NN + yi, N, kp.cdir[0], yi, kp.cdir[2], yk,
+                               kp.cdir[1], o);
+          }
           pinv_post<N, MODE>(kp, o, v);
 #pragma unroll
           for (int j = 0; j < N; ++j) Y2[at(LYX, yi, j, yk)] = v[j];
         }
       }
       __syncthreads();
+      Real ujz[R][N], upz[R][N];   // the update's inputs along the z-lines, loaded one stage early
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int zj = tb + r * NB, zi = ta;
+          if (N % R != 0 && zj >= N) break;
+          const int64_t gbase = cid * N3 + zj * N + zi;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            ujz[r][k] = __ldg(u + gbase + k * NN);
+            if (!ch.first) upz[r][k] = ch.u_prev[gbase + k * NN];
+          }
+        }
+      }
       if (active) {   // x: T^{-1}
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -679,8 +711,17 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
 #pragma unroll
           for (int k = 0; k < N; ++k) v[k] = X1[at(LXZ, zi, zj, k)];
           pinv_post<N, MODE>(kp, v, res[r]);
+          // three-term update, Eq. (11)
+          const int64_t gbase = cid * N3 + zj * N + zi;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            Real vv = fma((Real)ch.c_z, res[r][k], ujz[r][k]);
+            if (!ch.first) vv = fma((Real)ch.c_prev, ujz[r][k] - upz[r][k], vv);
+            ch.u_next[gbase + k * NN] = vv;
+          }
         }
       }
+      return;
     } else {
       // point Jacobi: diagonal along the x-lines, then to z-lines through smem
       Real* X1 = R1 + cslot * LXZ.CS;
