@@ -642,6 +642,13 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
 
   // ================================================================ Z^T
   double res[N];
+  double bz[MODE == KMODE_APPLY ? 1 : N];   // Chebyshev: b along the z-line, issued before the sweeps
+  if constexpr (MODE != KMODE_APPLY) {
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) bz[k] = __ldg(ch.b + cid * N3 + k * NN + zj * N + zi);
+    }
+  }
   if (active) {
     double v1[N], v2[N];
     ld_line<N, 0>(R1 + cslot * LZY.CS + at(LZY, zi, zj, 0), LZY.Pk, v1);
@@ -669,8 +676,9 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
   } else {
     if (active) {
 #pragma unroll
-      for (int k = 0; k < N; ++k) res[k] = __ldg(ch.b + gbase + k * NN) - res[k];
+      for (int k = 0; k < N; ++k) res[k] = bz[k] - res[k];
     }
+    double ujz[N], upz[N];   // the update's inputs
     if constexpr (MODE == KMODE_CHEBY_GL) {
       // z: T^-T -> R1 (ZY);  y: T^-T -> R2 (YX);  x: T^-T, diag, T^-1 -> R1 (YX);
       // y: T^-1 -> R2 (ZY);  z: T^-1 + update
@@ -681,6 +689,12 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
         st_line<N>(R1 + cslot * LZY.CS + at(LZY, zi, zj, 0), LZY.Pk, o);
       }
       __syncthreads();
+      double dx[N];   // the x stage's diagonal, loaded one stage early
+      if (active) {
+        const double* dv = ch.dinv + cid * N3 + (xq2 * N + xq1) * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) dx[i] = __ldg(dv + i);
+      }
       if (active) {
         double v[N], o[N];
         ld_line<N, 0>(R1 + cslot * LZY.CS + at(LZY, yi, 0, yq), LZY.Pj, v);
@@ -692,13 +706,19 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
         double v[N], o[N];
         ld_line<N, 0>(R2 + cslot * LYX.CS + at(LYX, 0, xq1, xq2), 1, v);
         eo_apply<N, 1>(qp.TiT, v, o);
-        const double* dv = ch.dinv + cid * N3 + (xq2 * N + xq1) * N;
 #pragma unroll
-        for (int i = 0; i < N; ++i) o[i] *= __ldg(dv + i);
+        for (int i = 0; i < N; ++i) o[i] *= dx[i];
         eo_apply<N, 1>(qp.Ti, o, v);
         st_line<N>(R1 + cslot * LYX.CS + at(LYX, 0, xq1, xq2), 1, v);
       }
       __syncthreads();
+      if (active) {   // update inputs along the z-line, one stage early
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          ujz[k] = __ldg(u + gbase + k * NN);
+          if (!ch.first) upz[k] = ch.u_prev[gbase + k * NN];
+        }
+      }
       if (active) {
         double v[N], o[N];
         ld_line<N, 0>(R1 + cslot * LYX.CS + at(LYX, yi, 0, yq), LYX.Pj, v);
@@ -714,17 +734,19 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
     } else {
       if (active) {
 #pragma unroll
-        for (int k = 0; k < N; ++k) res[k] *= __ldg(ch.dinv + gbase + k * NN);
+        for (int k = 0; k < N; ++k) {
+          res[k] *= __ldg(ch.dinv + gbase + k * NN);
+          ujz[k] = __ldg(u + gbase + k * NN);
+          if (!ch.first) upz[k] = ch.u_prev[gbase + k * NN];
+        }
       }
     }
     if (active) {
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        const int64_t gi = gbase + k * NN;
-        const double uj = __ldg(u + gi);
-        double v = fma(ch.c_z, res[k], uj);
-        if (!ch.first) v = fma(ch.c_prev, uj - ch.u_prev[gi], v);
-        ch.u_next[gi] = v;
+        double v = fma(ch.c_z, res[k], ujz[k]);
+        if (!ch.first) v = fma(ch.c_prev, ujz[k] - upz[k], v);
+        ch.u_next[gbase + k * NN] = v;
       }
     }
   }
