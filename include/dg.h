@@ -156,6 +156,15 @@ dg_status dg_apply_laplace(dg_mesh m, const double* u, double* y, int32_t flags,
 /* out = B^{x3} in per cell (see DG_BCHG_*); in == out is allowed. */
 dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, void* stream);
 
+/* y_host = A u_host with HOST vectors (n_local_dofs each): the host->device copy, the matvec
+ * and the device->host copy run in z-plane chunks overlapped on internal copy streams (the
+ * chunk being computed needs the first plane of the next one).  Stream-ordered on `stream`:
+ * y_host is complete when `stream` reaches the end of the call.  Pinned host memory is needed
+ * for the overlap (pageable memory works, copied synchronously by the driver).  Periodic z,
+ * several slabs or fewer than 4 planes use one whole-vector copy each way.  The library keeps
+ * two device vectors of staging per mesh after the first call. */
+dg_status dg_apply_laplace_host(dg_mesh m, const double* u_host, double* y_host, void* stream);
+
 /* Chebyshev iteration of Eq. (11), `degree` operator
  * applications, range [lo_frac, hi_frac] * lambda_max (paper: 0.06, 1.2).
  * b: right-hand side; x: in x_0, out x_degree; work2: 2 * n_local_dofs doubles

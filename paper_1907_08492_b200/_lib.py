@@ -69,6 +69,7 @@ SYMBOLS = {
     "dg_lanczos_lambda_max": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
                                              ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]),
     "dg_apply_laplace_f32": (ctypes.c_int, [ctypes.c_void_p] * 4),
+    "dg_apply_laplace_host": (ctypes.c_int, [ctypes.c_void_p] * 4),
     "dg_chebyshev_smooth_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                ctypes.c_void_p, ctypes.c_int32, ctypes.c_double,
                                                ctypes.c_double, ctypes.c_double, ctypes.c_int32,

@@ -216,6 +216,22 @@ class Mesh:
                "dg_apply_laplace")
         return y
 
+    def apply_laplace_host(self, u, y=None, stream=None):
+        """y = A u for HOST (CPU, ideally pinned) float64 tensors; the copies are overlapped with
+        the kernels inside the library (dg_apply_laplace_host).  Returns when `stream` is
+        synchronised by the caller (stream-ordered)."""
+        if not isinstance(u, torch.Tensor) or u.dtype != torch.float64 or u.is_cuda or not u.is_contiguous():
+            raise TypeError("u must be a contiguous CPU float64 tensor")
+        if y is None:
+            y = torch.empty(self.n_local_dofs, dtype=torch.float64, pin_memory=u.is_pinned())
+        if y.dtype != torch.float64 or y.is_cuda or not y.is_contiguous() or y.numel() < self.n_local_dofs:
+            raise TypeError("y must be a contiguous CPU float64 tensor of n_local_dofs")
+        if u.numel() < self.n_local_dofs:
+            raise ValueError("u too short")
+        _check(lib().dg_apply_laplace_host(self._h, ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                           _stream(stream)), "dg_apply_laplace_host")
+        return y
+
     def apply_laplace_f32(self, u, y=None, stream=None):
         """y = A u in single precision (Cartesian meshes, single slab; SURVEY.md §8(f) NEXT#3)."""
         f32 = torch.float32

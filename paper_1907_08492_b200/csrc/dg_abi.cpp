@@ -221,6 +221,12 @@ struct dg_mesh_s {
   bool kpf_ok = false;
   float* d_dinv_gl_f = nullptr;
   float* d_dinv_pj_f = nullptr;
+  // host-buffer apply (dg_apply_laplace_host): device staging, copy streams, per-chunk events
+  double* d_hu = nullptr;
+  double* d_hy = nullptr;
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  std::vector<cudaEvent_t> ev_h2d, ev_comp;
+  cudaEvent_t ev_done = nullptr;
 };
 
 namespace {
@@ -658,6 +664,13 @@ dg_status dg_mesh_destroy(dg_mesh m) {
   cudaFree(m->d_dot);
   cudaFree(m->d_dinv_gl_f);
   cudaFree(m->d_dinv_pj_f);
+  cudaFree(m->d_hu);
+  cudaFree(m->d_hy);
+  for (cudaEvent_t e : m->ev_h2d) cudaEventDestroy(e);
+  for (cudaEvent_t e : m->ev_comp) cudaEventDestroy(e);
+  if (m->ev_done) cudaEventDestroy(m->ev_done);
+  if (m->h2d_stream) cudaStreamDestroy(m->h2d_stream);
+  if (m->d2h_stream) cudaStreamDestroy(m->d2h_stream);
   cudaFree(m->d_recv_lo);
   cudaFree(m->d_recv_hi);
   cudaFree(m->d_send_lo);
@@ -1264,6 +1277,96 @@ dg_status dg_chebyshev_smooth_f32(dg_mesh m, const float* b, float* x, float* wo
   }
   if (where[degree] != 0)
     CUDA_TRY(cudaMemcpyAsync(x, buf[where[degree]], sizeof(float) * (size_t)nd, cudaMemcpyDeviceToDevice, s));
+  return DG_OK;
+}
+
+}  // extern "C"
+
+// ================================================================ host-buffer matvec
+// y_host = A u_host with the host<->device copies inside the call, overlapped plane-chunk by
+// plane-chunk with the kernels: H2D of chunk c+1 on one copy stream while chunk c computes
+// (it needs the first plane of chunk c+1 as its z-neighbour) and the D2H of chunk c-1 drains
+// on a second copy stream.  Pinned host memory makes the copies asynchronous (pageable memory
+// is accepted and copied synchronously by the driver).
+namespace {
+
+dg_status launch_apply_range(dg_mesh m, bool kron, const double* u, double* y, int zb, int ze, cudaStream_t s) {
+  if (ze <= zb) return DG_OK;
+  GridArgs g = grid_args(m, zb, ze);
+  ChebyArgs ch{};
+  cudaError_t e;
+  if (kron && kron_v4(m->n))
+    e = launch_kron4(m->n, m->NL, KMODE_APPLY, m->kp, g, u, y, ch, s);
+  else if (kron)
+    e = launch_kron(m->n, m->NL, KMODE_APPLY, m->kp, g, u, y, ch, s);
+  else if (quad_v3(m->n, m->geom))
+    e = launch_quad3(m->n, m->NL, m->geom, KMODE_APPLY, m->qp, m->ga, g, u, y, ch, s);
+  else
+    e = launch_quad(m->n, m->NL, m->geom, KMODE_APPLY, m->qp, m->ga, g, u, y, ch, s);
+  return post_launch(m, e, "apply", s);
+}
+
+}  // namespace
+
+extern "C" {
+
+dg_status dg_apply_laplace_host(dg_mesh m, const double* u_host, double* y_host, void* stream) {
+  if (!m || !u_host || !y_host) return fail(DG_ERR_PARAM, "NULL argument");
+  if (u_host == y_host) return fail(DG_ERR_PARAM, "u and y alias");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nd = m->ndofs_local;
+  const size_t bytes = sizeof(double) * (size_t)std::max<int64_t>(nd, 1);
+  if (!m->d_hu) {
+    CUDA_TRY(cudaMalloc(&m->d_hu, bytes));
+    CUDA_TRY(cudaMalloc(&m->d_hy, bytes));
+    CUDA_TRY(cudaStreamCreateWithFlags(&m->h2d_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&m->d2h_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&m->ev_done, cudaEventDisableTiming));
+  }
+  const bool kron = m->cartesian;
+  const bool zwrap = m->zlo == ZSRC_LOCAL || m->zhi == ZSRC_LOCAL;   // periodic single slab
+  const bool halo = m->zlo == ZSRC_HALO || m->zhi == ZSRC_HALO;
+  if (zwrap || halo || m->nz < 4) {   // whole-vector path (the exchange needs all planes first)
+    CUDA_TRY(cudaMemcpyAsync(m->d_hu, u_host, sizeof(double) * nd, cudaMemcpyHostToDevice, s));
+    ChebyArgs ch{};
+    dg_status st = run_pass(m, KMODE_APPLY, kron, m->d_hu, m->d_hy, ch, false, s);
+    if (st != DG_OK) return st;
+    CUDA_TRY(cudaMemcpyAsync(y_host, m->d_hy, sizeof(double) * nd, cudaMemcpyDeviceToHost, s));
+    return DG_OK;
+  }
+  const int64_t plane = (int64_t)m->N[0] * m->N[1] * m->n * m->n * m->n;
+  const int nchunk = std::min(8, m->nz / 2);
+  while ((int)m->ev_h2d.size() < nchunk) {
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    m->ev_h2d.push_back(a);
+    m->ev_comp.push_back(b);
+  }
+  auto zb = [&](int c) { return (int)((int64_t)m->nz * c / nchunk); };
+  // everything before this call on `stream` happens first
+  CUDA_TRY(cudaEventRecord(m->ev_done, s));
+  CUDA_TRY(cudaStreamWaitEvent(m->h2d_stream, m->ev_done, 0));
+  CUDA_TRY(cudaStreamWaitEvent(m->d2h_stream, m->ev_done, 0));
+  for (int c = 0; c < nchunk; ++c) {
+    const int64_t o = zb(c) * plane, cnt = (int64_t)(zb(c + 1) - zb(c)) * plane;
+    CUDA_TRY(cudaMemcpyAsync(m->d_hu + o, u_host + o, sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                             m->h2d_stream));
+    CUDA_TRY(cudaEventRecord(m->ev_h2d[c], m->h2d_stream));
+  }
+  for (int c = 0; c < nchunk; ++c) {
+    // planes [zb(c), zb(c+1)) need the first plane of the next chunk
+    CUDA_TRY(cudaStreamWaitEvent(s, m->ev_h2d[std::min(c + 1, nchunk - 1)], 0));
+    dg_status st = launch_apply_range(m, kron, m->d_hu, m->d_hy, zb(c), zb(c + 1), s);
+    if (st != DG_OK) return st;
+    CUDA_TRY(cudaEventRecord(m->ev_comp[c], s));
+    CUDA_TRY(cudaStreamWaitEvent(m->d2h_stream, m->ev_comp[c], 0));
+    const int64_t o = zb(c) * plane, cnt = (int64_t)(zb(c + 1) - zb(c)) * plane;
+    CUDA_TRY(cudaMemcpyAsync(y_host + o, m->d_hy + o, sizeof(double) * cnt, cudaMemcpyDeviceToHost,
+                             m->d2h_stream));
+  }
+  CUDA_TRY(cudaEventRecord(m->ev_done, m->d2h_stream));
+  CUDA_TRY(cudaStreamWaitEvent(s, m->ev_done, 0));
   return DG_OK;
 }
 

@@ -439,3 +439,24 @@ def test_rows_longer_than_a_block(p, nc, bcx):
             x = _dev(u)
             m.chebyshev_smooth(_dev(b), x, 2.4, degree=2)
             assert _rel(x.cpu().numpy(), ref) <= TOL, geom
+
+
+@pytest.mark.parametrize("spec", [
+    MeshSpec(degree=5, n_cells=(7, 5, 11), seed=170),                                         # chunked
+    MeshSpec(degree=3, n_cells=(4, 3, 9), bc=("periodic", "dirichlet", "periodic"), seed=171),  # z-wrap
+    MeshSpec(degree=4, n_cells=(3, 3, 8), deform_amp=0.04, geometry="per_qpoint", seed=172),   # k_quad3
+    MeshSpec(degree=2, n_cells=(3, 2, 3), seed=173),                                          # < 4 planes
+], ids=["chunked", "zwrap", "curved", "few-planes"])
+def test_apply_host_buffers(spec):
+    """dg_apply_laplace_host (HOST vectors, copies overlapped with the kernels) equals the
+    device-vector matvec bit for bit; pinned and pageable host memory."""
+    _needs_gpu()
+    u = uniform_vector(spec.n_dofs, spec.seed)
+    m = _gpu_mesh(spec)
+    yd = m.apply_laplace(_dev(u)).cpu().numpy()
+    for pinned in (True, False):
+        uh = torch.from_numpy(u).pin_memory() if pinned else torch.from_numpy(u.copy())
+        yh = m.apply_laplace_host(uh)
+        torch.cuda.synchronize()
+        assert np.array_equal(yh.numpy(), yd), pinned
+    assert _rel(yd, _oracle(spec).apply(u)) <= TOL
