@@ -76,8 +76,12 @@ struct K4Layout {
   // R1: T -> B -> (P^-1: z->y, x->z) -> output;  R2: A -> C -> (P^-1: x->z, y->x)
   static constexpr int S1 = imax(imax(imax(ZY.CS, YX.CS), OUT.CS), USE_XZ ? XZ.CS : 0);
   static constexpr int S2 = imax(imax(ZY.CS, YX.CS), USE_XZ ? XZ.CS : 0);
-  static constexpr int PG = N | 1;
-  static constexpr int GYC = 2 * NL * N * PG;          // y-ghost rows per cell [f][l][k][i]
+  static constexpr int PG = N | 1;                     // x-halo row pitch
+  // y-ghost rows per cell, addr (f*NL + l)*GFS + k*GPG + i (tools/smem_gy_search.py for NL = 2)
+  static constexpr int GPG = N;
+  static constexpr int GFS = NL == 2 ? (N == 3 ? 22 : (N == 4 ? 20 : (N == 5 ? 37 : (N == 6 ? 38 : (N == 7 ? 55 : (N == 8 ? 72 : 89))))))
+                                     : N * N + 2;
+  static constexpr int GYC = 2 * NL * GFS + (N == 3 && NL == 2 ? 1 : 0);
   static constexpr int HS = NL * N * PG;               // one x-halo field [l][k][j]
   static constexpr int doubles() { return CPB * (S1 + S2 + GYC) + 2 * 2 * HS; }
   static constexpr int bytes() { return doubles() * 8; }
@@ -157,7 +161,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
   constexpr int R = Lay::R, NB = Lay::NB, TPC = Lay::TPC, CPB = Lay::CPB;
   constexpr int NN = N * N, N3 = N * NN;
   constexpr Lay3 LZY = Lay::ZY, LYX = Lay::YX, LXZ = Lay::XZ, LOUT = Lay::OUT;
-  constexpr int PG = Lay::PG;
+  constexpr int PG = Lay::PG, GPG = Lay::GPG, GFS = Lay::GFS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real* smem = reinterpret_cast<Real*>(smem_raw);
   Real* R1 = smem;
@@ -222,7 +226,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
   const int nyj = ncell * NYJ;
   const int nh0 = h0 >= 0 ? NL * N : 0, nh1 = h1 >= 0 ? NL * N : 0;
   const int njobs = nyj + nh0 + nh1;
-  auto job_target = [&](int job, const Real*& src, Real*& dst) {
+  auto job_target = [&](int job, const Real*& src, Real*& dst, int& ds) {
     if (job < nyj) {
       const int c = job / NYJ, jj = job - c * NYJ;
       const int f = jj / (NL * N), l = (jj / N) % NL, i = jj % N;
@@ -233,7 +237,8 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       }
       const int jl = f ? l : N - NL + l;
       src = u + (((int64_t)cz * g.Ny + nrow) * g.Nx + cx0 + c) * N3 + jl * N + i;
-      dst = GYb + c * Lay::GYC + ((f * NL + l) * N) * PG + i;
+      dst = GYb + c * Lay::GYC + (f * NL + l) * GFS + i;
+      ds = GPG;
     } else {
       const int hj = job - nyj;
       const int h = hj < nh0 ? 0 : 1;
@@ -242,6 +247,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       const int il = h == 0 ? N - NL + l : l;
       src = u + (rowcell + (h ? h1 : h0)) * N3 + j * N + il;
       dst = HX + ((h * 2 + 0) * NL + l) * N * PG + j;
+      ds = PG;
     }
   };
   // next plane's tile (same x-run and row) into L2: its block runs about one wave later
@@ -257,8 +263,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
   // the first job's loads are issued together with the own z-lines
   const Real* jsrc = nullptr;
   Real* jdst = nullptr;
+  int jds = PG;
   Real jv[N];
-  if (btid < njobs) job_target(btid, jsrc, jdst);
+  if (btid < njobs) job_target(btid, jsrc, jdst, jds);
   if (jsrc) {
 #pragma unroll
     for (int k = 0; k < N; ++k) jv[k] = __ldg(jsrc + k * NN);
@@ -298,14 +305,15 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
     Real o[N];
     eo_apply<N, 1>(kp.M, jv, o);
 #pragma unroll
-    for (int k = 0; k < N; ++k) jdst[k * PG] = o[k];
+    for (int k = 0; k < N; ++k) jdst[k * jds] = o[k];
   }
 #pragma unroll 1
   for (int job = btid + BT; job < njobs; job += BT) {
     const Real* src;
     Real* dst;
-    job_target(job, src, dst);
-    if (src) mass_line<N>(kp.M, src, NN, dst, PG);
+    int ds = PG;
+    job_target(job, src, dst, ds);
+    if (src) mass_line<N>(kp.M, src, NN, dst, ds);
   }
   __syncthreads();
 
@@ -328,8 +336,8 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
         Real gym[NL], gyp[NL];
 #pragma unroll
         for (int l = 0; l < NL; ++l) {
-          gym[l] = ym_row >= 0 ? GY[((0 * NL + l) * N + yk) * PG + yi] : -tl[NL - 1 - l];
-          gyp[l] = yp_row >= 0 ? GY[((1 * NL + l) * N + yk) * PG + yi] : -tl[N - 1 - l];
+          gym[l] = ym_row >= 0 ? GY[(0 * NL + l) * GFS + yk * GPG + yi] : -tl[NL - 1 - l];
+          gyp[l] = yp_row >= 0 ? GY[(1 * NL + l) * GFS + yk * GPG + yi] : -tl[N - 1 - l];
         }
         const auto st = eo_split<N>(tl);
         eo_mul2<N, 1>(kp.M, eo_split<N>(al), kp.L[1], st, bl[r]);
