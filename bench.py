@@ -359,8 +359,14 @@ def run_ours(a, rank, world, local_rank):
     dom_name = max(dom, key=lambda k: dom[k][1])
     dom = {k: v if v[1] > 0 else [0.0, 1e-30] for k, v in dom.items()}
     ach = dom[dom_name][0] / (dom[dom_name][1] * 1e-3) / 1e9 / world   # per-GPU GB/s
-    kname = "k_kron4" if all(sp.geometry == "constant" and sp.deform_amp == 0 for sp in specs) else "k_quad"
-    kernel = {"matvec": f"{kname}<APPLY>", "basis_change": "k_bchg",
+    if all(sp.geometry == "constant" and sp.deform_amp == 0 for sp in specs):
+        kname = "k_kron4"
+    elif all(sp.geometry in ("constant", "per_qpoint") for sp in specs) and os.environ.get("DG_QUAD") != "1":
+        kname = "k_quad3"
+    else:
+        kname = "k_quad"
+    bname = "k_bchg" if os.environ.get("DG_BCHG") == "1" or any(p < 2 or p > 8 for p in degrees) else "k_bchg4"
+    kernel = {"matvec": f"{kname}<APPLY>", "basis_change": bname,
               "chebyshev_step": f"{kname}<CHEBY_GL>"}[dom_name]
     traffic, traffic_note = measured_traffic(a.workload, kernel, degrees, dom[dom_name][0] / max(1, a.steps))
     roofline = {"bound": "hbm", "kernel": kernel,
