@@ -120,6 +120,10 @@ cudaError_t launch_kron4(int n, int NL, int mode, const KronParams& kp, const Gr
                          const double* u, double* y, const ChebyArgs& ch, cudaStream_t s);
 cudaError_t launch_kron4_f32(int n, int NL, int mode, const KronParamsF& kp, const GridArgs& g,
                              const float* u, float* y, const ChebyArgsF& ch, cudaStream_t s);
+// z-first basis change (k_kron4.cu), n = 3..9; in == out is NOT allowed (z-lines are read
+// while other blocks write)
+cudaError_t launch_basis_change4(int n, const BchgParams& bp, const double* in, double* out, int64_t ncells,
+                                 cudaStream_t s);
 cudaError_t launch_basis_change(int n, const BchgParams& bp, const double* in, double* out,
                                 int64_t ncells, cudaStream_t s);
 // diagonal of a Cartesian Kronecker operator: d[i,j,k] = sum_d c_d prod(1D diagonals)

@@ -834,6 +834,110 @@ cudaError_t launch_nl(int NL, int mode, const KronParamsT<Real>& kp, const GridA
   return cudaErrorInvalidValue;
 }
 
+// Basis change v_K = (B (x) B (x) B) u_K per cell (Eq. (12)) in the same
+// z-first thread mapping and transposition layouts as k_kron4: z-lines straight from HBM
+// (coalesced), z -> y -> x transposes through two smem fields, output along the x-lines
+// (128-bit stores for even n, smem-staged coalesced stores for odd n).  HBM-bound, 16 B/DoF.
+template <int N>
+__global__ void __launch_bounds__(K4Layout<N, 2>::CPB * K4Layout<N, 2>::TPC)
+k_bchg4(const __grid_constant__ BchgParams bp, const double* __restrict__ in, double* __restrict__ out,
+        int64_t ncells) {
+  using Lay = K4Layout<N, 2>;
+  constexpr int R = Lay::R, NB = Lay::NB, CPB = Lay::CPB;
+  constexpr int NN = N * N, N3 = N * NN;
+  constexpr Lay3 LZY = Lay::ZY, LYX = Lay::YX, LOUT = Lay::OUT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* R1 = reinterpret_cast<double*>(smem_raw);
+  double* R2 = R1 + CPB * Lay::S1;
+  const int ta = threadIdx.x, cslot = threadIdx.y / NB, tb = threadIdx.y - cslot * NB;
+  const int64_t cell0 = (int64_t)blockIdx.x * CPB;
+  const int ncell = (int)(ncells - cell0 < CPB ? ncells - cell0 : CPB);
+  const bool active = cslot < ncell;
+  const int64_t cid = cell0 + cslot;
+  if (active) {   // z
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int zj = tb + r * NB, zi = ta;
+      if (N % R != 0 && zj >= N) break;
+      double v[N], o[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) v[k] = __ldg(in + cid * N3 + k * NN + zj * N + zi);
+      eo_apply<N, 1>(bp.B, v, o);
+      double* W = R1 + cslot * LZY.CS;
+#pragma unroll
+      for (int k = 0; k < N; ++k) W[at(LZY, zi, zj, k)] = o[k];
+    }
+  }
+  __syncthreads();
+  if (active) {   // y
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int yk = tb + r * NB, yi = ta;
+      if (N % R != 0 && yk >= N) break;
+      double v[N], o[N];
+      const double* Rd = R1 + cslot * LZY.CS;
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = Rd[at(LZY, yi, j, yk)];
+      eo_apply<N, 1>(bp.B, v, o);
+      double* W = R2 + cslot * LYX.CS;
+#pragma unroll
+      for (int j = 0; j < N; ++j) W[at(LYX, yi, j, yk)] = o[j];
+    }
+  }
+  __syncthreads();
+  double res[R][N];
+  if (active) {   // x
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int xk = tb + r * NB, xj = ta;
+      if (N % R != 0 && xk >= N) break;
+      double v[N];
+      const double* Rd = R2 + cslot * LYX.CS;
+#pragma unroll
+      for (int i = 0; i < N; ++i) v[i] = Rd[at(LYX, i, xj, xk)];
+      eo_apply<N, 1>(bp.B, v, res[r]);
+      if constexpr (N % 2 == 0) {
+        double* o = out + cid * N3 + (xk * N + xj) * N;
+#pragma unroll
+        for (int i = 0; i < N; i += 2) *reinterpret_cast<double2*>(o + i) = make_double2(res[r][i], res[r][i + 1]);
+      }
+    }
+  }
+  if constexpr (N % 2 == 1) {   // stage in R1 (free since the y stage) for coalesced stores
+    double* O = R1 + cslot * LOUT.CS;
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int xk = tb + r * NB, xj = ta;
+        if (N % R != 0 && xk >= N) break;
+#pragma unroll
+        for (int i = 0; i < N; ++i) O[at(LOUT, i, xj, xk)] = res[r][i];
+      }
+    }
+    __syncthreads();
+    if (active) {
+      double* o = out + cid * N3;
+#pragma unroll
+      for (int q = 0; q < (NN + NB - 1) / NB; ++q) {
+        const int rowi = tb + q * NB;
+        if (NN % NB == 0 || rowi < NN) o[rowi * N + ta] = O[rowi * LOUT.Pj + ta];
+      }
+    }
+  }
+}
+
+template <int N>
+cudaError_t launch_bchg4_n(const BchgParams& bp, const double* in, double* out, int64_t ncells, cudaStream_t s) {
+  using Lay = K4Layout<N, 2>;
+  if (ncells <= 0) return cudaSuccess;
+  const size_t smem = (size_t)Lay::CPB * (Lay::S1 + Lay::S2) * sizeof(double);
+  auto kern = k_bchg4<N>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)((ncells + Lay::CPB - 1) / Lay::CPB), dim3(N, Lay::NB * Lay::CPB), smem, s>>>(bp, in, out, ncells);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 // n in 3..9 (p = 2..8); other degrees use k_kron.cu
@@ -864,4 +968,20 @@ cudaError_t launch_kron4_f32(int n, int NL, int mode, const KronParamsF& kp, con
   return launch_kron4_t<float>(n, NL, mode, kp, g, u, y, ch, s);
 }
 
+}  // namespace dgb
+
+namespace dgb {
+cudaError_t launch_basis_change4(int n, const BchgParams& bp, const double* in, double* out, int64_t ncells,
+                                 cudaStream_t s) {
+  switch (n) {
+    case 3: return launch_bchg4_n<3>(bp, in, out, ncells, s);
+    case 4: return launch_bchg4_n<4>(bp, in, out, ncells, s);
+    case 5: return launch_bchg4_n<5>(bp, in, out, ncells, s);
+    case 6: return launch_bchg4_n<6>(bp, in, out, ncells, s);
+    case 7: return launch_bchg4_n<7>(bp, in, out, ncells, s);
+    case 8: return launch_bchg4_n<8>(bp, in, out, ncells, s);
+    case 9: return launch_bchg4_n<9>(bp, in, out, ncells, s);
+  }
+  return cudaErrorInvalidValue;
+}
 }  // namespace dgb

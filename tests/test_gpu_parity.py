@@ -140,6 +140,19 @@ def test_basis_change(p, op):
     assert _rel(w.cpu().numpy(), ref) <= TOL
 
 
+@pytest.mark.parametrize("p", [2, 3, 5, 6, 8])
+def test_basis_change_many_blocks(p):
+    """z-first k_bchg4 over several blocks with a ragged last block (7*5*3 = 105 cells)."""
+    _needs_gpu()
+    from oracle import smoother as sm
+    spec = MeshSpec(degree=p, n_cells=(7, 5, 3), seed=60 + p)
+    u = uniform_vector(spec.n_dofs, spec.seed)
+    m = _gpu_mesh(spec)
+    for op in ("T", "TinvT"):
+        ref = sm.basis_change(p, u, op)
+        assert _rel(m.basis_change(op, _dev(u)).cpu().numpy(), ref) <= TOL
+
+
 @pytest.mark.parametrize("p", [1, 2, 4, 7])
 @pytest.mark.parametrize("basis", ["hermite", "gl"])
 def test_inverse_diagonal(p, basis):
