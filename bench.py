@@ -365,7 +365,7 @@ def run_ours(a, rank, world, local_rank):
         kname = "k_quad3"
     else:
         kname = "k_quad"
-    bname = "k_bchg" if os.environ.get("DG_BCHG") == "1" or any(p < 2 or p > 8 for p in degrees) else "k_bchg4"
+    bname = "k_bchg4" if os.environ.get("DG_BCHG") == "4" else "k_bchg"   # k_bchg4 default only at p=2, 8
     kernel = {"matvec": f"{kname}<APPLY>", "basis_change": bname,
               "chebyshev_step": f"{kname}<CHEBY_GL>"}[dom_name]
     traffic, traffic_note = measured_traffic(a.workload, kernel, degrees, dom[dom_name][0] / max(1, a.steps))

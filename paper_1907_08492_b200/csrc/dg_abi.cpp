@@ -799,13 +799,15 @@ dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, 
   BchgParams bp{};
   pack_eo(B, n, bp.B);
   cudaStream_t s = (cudaStream_t)stream;
-  // z-first kernel unless in == out (it reads each cell before any block writes it only for
-  // the cell-staged k_bchg, which supports in-place) or DG_BCHG=1
+  // k_bchg (cell-staged, in-place capable) or the z-first k_bchg4 (out of place only).
+  // Default by measurement (C4, tools/bchg_ab.py): k_bchg4 for n = 3 and 9, k_bchg otherwise;
+  // DG_BCHG=1 / DG_BCHG=4 force one of them.
   static const int v = [] {
     const char* e = std::getenv("DG_BCHG");
-    return e ? std::atoi(e) : 4;
+    return e ? std::atoi(e) : 0;
   }();
-  if (v != 1 && in != out && kron4_supported(n))
+  const bool use4 = v == 4 || (v == 0 && (n == 3 || n == 9));
+  if (use4 && in != out && kron4_supported(n))
     return post_launch(m, launch_basis_change4(n, bp, in, out, m->ncells_local, s), "basis_change", s);
   return post_launch(m, launch_basis_change(n, bp, in, out, m->ncells_local, s), "basis_change", s);
 }

@@ -9,7 +9,7 @@
 // of the neighbour next to the face for the Hermite-like basis).
 //
 // Thread mapping: a block is a run of CPB cells of one x-row (grid = x-runs x rows x
-// planes); thread (a, b', cell) = (threadIdx.x, threadIdx.y % NB, threadIdx.y / NB) owns the R lines (a, b' + r*NB),
+// planes); thread t = cell*TPCP + b'*n + a (TPCP = n*NB, or padded, K4C::TP) owns the R lines (a, b' + r*NB),
 // NB = ceil(n/R), of every sweep direction, so per-thread setup and the coefficient
 // loads are amortised over R lines.  Sweeping z first lets the own data and the raw
 // z-neighbour layers stream from HBM along coalesced z-lines:
@@ -49,17 +49,21 @@ struct Lay3 {
 // addr = i + j*Pj + k*Pk + cell*CS chosen by tools/smem_layout_search6.py (half-warp model)
 // (ZY: z-write/y-read, YX: y-write/x-read, XZ: x-write/z-read).
 template <int N, int ALT = 0> struct K4C;
-template <> struct K4C<3> { static constexpr int R = 1, CPB = 32; static constexpr Lay3 ZY{3, 19, 57}, YX{3, 9, 27}, XZ{3, 18, 57}; };
-template <> struct K4C<4> { static constexpr int R = 2, CPB = 30; static constexpr Lay3 ZY{4, 20, 88}, YX{5, 20, 88}, XZ{5, 20, 84}; };
-template <> struct K4C<5> { static constexpr int R = 2, CPB = 16; static constexpr Lay3 ZY{5, 26, 143}, YX{5, 25, 134}, XZ{5, 25, 139}; };
-template <> struct K4C<6> { static constexpr int R = 1, CPB = 8; static constexpr Lay3 ZY{6, 38, 228}, YX{9, 54, 324}, XZ{11, 66, 402}; };
-template <> struct K4C<7> { static constexpr int R = 2, CPB = 10; static constexpr Lay3 ZY{7, 55, 396}, YX{7, 56, 392}, XZ{7, 49, 344}; };
-template <> struct K4C<8> { static constexpr int R = 1, CPB = 4; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{12, 97, 776}; };
-template <> struct K4C<9> { static constexpr int R = 1, CPB = 3; static constexpr Lay3 ZY{9, 89, 801}, YX{9, 85, 765}, XZ{9, 81, 729}; };
+template <> struct K4C<3> { static constexpr int R = 1, CPB = 32, TP = 0, XSW = 0; static constexpr Lay3 ZY{3, 19, 57}, YX{3, 9, 27}, XZ{3, 18, 57}; };
+template <> struct K4C<4> { static constexpr int R = 2, CPB = 30, TP = 0, XSW = 0; static constexpr Lay3 ZY{4, 20, 88}, YX{5, 20, 88}, XZ{5, 20, 84}; };
+template <> struct K4C<5> { static constexpr int R = 2, CPB = 16, TP = 0, XSW = 0; static constexpr Lay3 ZY{5, 26, 143}, YX{5, 25, 134}, XZ{5, 25, 139}; };
+template <> struct K4C<6> { static constexpr int R = 1, CPB = 8, TP = 0, XSW = 0; static constexpr Lay3 ZY{6, 38, 228}, YX{9, 54, 324}, XZ{11, 66, 402}; };
+template <> struct K4C<7> { static constexpr int R = 2, CPB = 10, TP = 0, XSW = 0; static constexpr Lay3 ZY{7, 55, 396}, YX{7, 56, 392}, XZ{7, 49, 344}; };
+template <> struct K4C<8> { static constexpr int R = 1, CPB = 4, TP = 0, XSW = 0; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{12, 97, 776}; };
+template <> struct K4C<9> { static constexpr int R = 1, CPB = 3, TP = 0, XSW = 0; static constexpr Lay3 ZY{9, 89, 801}, YX{9, 85, 765}, XZ{9, 81, 729}; };
 // alternates (DG_K4_ALT=1): two lines per thread
-template <> struct K4C<6, 1> { static constexpr int R = 2, CPB = 16; static constexpr Lay3 ZY{6, 38, 242}, YX{9, 54, 338}, XZ{6, 36, 217}; };
-template <> struct K4C<8, 1> { static constexpr int R = 2, CPB = 8; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{9, 72, 576}; };
-template <int N> struct K4HasAlt { static constexpr bool value = N == 6 || N == 8; };
+template <> struct K4C<6, 1> { static constexpr int R = 2, CPB = 16, TP = 0, XSW = 0; static constexpr Lay3 ZY{6, 38, 242}, YX{9, 54, 338}, XZ{6, 36, 217}; };
+template <> struct K4C<8, 1> { static constexpr int R = 2, CPB = 8, TP = 0, XSW = 0; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{9, 72, 576}; };
+// n = 5 alternate: 16 threads per cell (one idle) so that a half-warp never straddles two cells,
+// and the x stage maps thread (a, b) to line (j, k) = (b + r NB, a); with these the Y/X
+// transposes are bank-conflict free (tools/smem_layout_search7.py / smem_ktable_search.py)
+template <> struct K4C<5, 1> { static constexpr int R = 2, CPB = 16, TP = 16, XSW = 1; static constexpr Lay3 ZY{5, 27, 135}, YX{7, 37, 185}, XZ{5, 31, 155}; };
+template <int N> struct K4HasAlt { static constexpr bool value = N == 5 || N == 6 || N == 8; };
 
 constexpr int imax(int a, int b) { return a > b ? a : b; }
 
@@ -69,7 +73,9 @@ struct K4Layout {
   static constexpr bool USE_XZ = MODE == KMODE_CHEBY_PJ || (N % 2 == 1 && MODE != KMODE_APPLY);
   static constexpr int R = K4C<N, ALT>::R, CPB = K4C<N, ALT>::CPB;
   static constexpr int NB = (N + R - 1) / R;          // thread rows per cell
-  static constexpr int TPC = N * NB;                   // threads per cell
+  static constexpr int TPC = N * NB;                   // working threads per cell
+  static constexpr int TPCP = K4C<N, ALT>::TP ? K4C<N, ALT>::TP : TPC;   // incl. idle padding
+  static constexpr bool XSW = K4C<N, ALT>::XSW;       // x stage: line (j,k) = (b', a) instead of (a, b')
   static constexpr Lay3 ZY = K4C<N, ALT>::ZY, YX = K4C<N, ALT>::YX, XZ = K4C<N, ALT>::XZ;
   static constexpr int P = N | 1;                      // output staging row pitch
   static constexpr Lay3 OUT{P, N * P, N * N * P};
@@ -93,7 +99,7 @@ template <int N, int NL, int ALT, typename Real, int MODE>
 constexpr int k4_min_blocks() {
   using L = K4Layout<N, NL, ALT, MODE>;
   constexpr int b = (227 * 1024) / (L::doubles() * (int)sizeof(Real));
-  constexpr int t = 2048 / (L::CPB * L::TPC);
+  constexpr int t = 2048 / (L::CPB * L::TPCP);
   constexpr int m = b < t ? b : t;
   constexpr int cap = sizeof(Real) == 4 ? (N == 7 ? 3 : 5) : (N == 3 ? 4 : 3);   // measured (r1)
   return m < 1 ? 1 : (m > cap ? cap : m);
@@ -152,7 +158,7 @@ template <> struct Vec2<double> { using type = double2; };
 template <> struct Vec2<float> { using type = float2; };
 
 template <int N, int NL, int MODE, int OUTD, int ALT, typename Real>
-__global__ void __launch_bounds__(K4Layout<N, NL, ALT>::CPB * K4Layout<N, NL, ALT>::TPC,
+__global__ void __launch_bounds__(K4Layout<N, NL, ALT>::CPB * K4Layout<N, NL, ALT>::TPCP,
                                   (k4_min_blocks<N, NL, ALT, Real, MODE>()))
 k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ GridArgs g,
         const Real* __restrict__ u, Real* __restrict__ y, const __grid_constant__ ChebyArgsT<Real> ch) {
@@ -169,12 +175,18 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
   Real* GYb = R2 + CPB * Lay::S2;
   Real* HX = GYb + CPB * Lay::GYC;   // [h][field: 0 = t, 1 = c][l][k][j]
 
-  const int ta = threadIdx.x, cslot = threadIdx.y / NB, tb = threadIdx.y - cslot * NB;
+  constexpr int TPCP = Lay::TPCP;
+  constexpr bool XSW = Lay::XSW;
+  // block (n, NB*CPB) unpadded; 1D (CPB*TPCP) when padded: tb >= NB is an idle padding
+  // thread (jobs only)
+  const int cslot = TPCP == TPC ? threadIdx.y / NB : threadIdx.x / TPCP;
+  const int tb = TPCP == TPC ? threadIdx.y - cslot * NB : (threadIdx.x - cslot * TPCP) / N;
+  const int ta = TPCP == TPC ? threadIdx.x : threadIdx.x - cslot * TPCP - tb * N;
   const int cx0 = blockIdx.x * CPB;
   const int cy = blockIdx.y;
   const int cz = g.zbeg + blockIdx.z;
   const int ncell = g.Nx - cx0 < CPB ? g.Nx - cx0 : CPB;
-  const bool active = cslot < ncell;
+  const bool active = cslot < ncell && (TPCP == TPC || tb < NB);
   const int cx = cx0 + cslot;
   const int64_t plane = (int64_t)g.Nx * g.Ny;
   const int64_t rowcell = ((int64_t)cz * g.Ny + cy) * g.Nx;
@@ -221,8 +233,8 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
   //   then NL*N x-halo z-lines (l, j) per needed block edge -> HT[h][l][k][j]
   // Every job is "load a z-line (stride n^2), apply M_z, store with stride PG".
   constexpr int NYJ = 2 * NL * N;
-  constexpr int BT = CPB * TPC;
-  const int btid = threadIdx.x + N * threadIdx.y;
+  constexpr int BT = CPB * TPCP;
+  const int btid = TPCP == TPC ? threadIdx.x + N * threadIdx.y : threadIdx.x;
   const int nyj = ncell * NYJ;
   const int nh0 = h0 >= 0 ? NL * N : 0, nh1 = h1 >= 0 ? NL * N : 0;
   const int njobs = nyj + nh0 + nh1;
@@ -347,9 +359,8 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       }
     }
     {   // halo jobs: HC[h][l][k][j] = M_y HT[h][l][k][:], spread over the block
-      const int btid = threadIdx.x + N * threadIdx.y;
       const int nh0 = h0 >= 0 ? NL * N : 0, nh1 = h1 >= 0 ? NL * N : 0;
-      for (int job = btid; job < nh0 + nh1; job += CPB * TPC) {
+      for (int job = btid; job < nh0 + nh1; job += BT) {
         const int h = job < nh0 ? 0 : 1;
         const int q = job - (h ? nh0 : 0);
         const int l = q / N, k = q - l * N;
@@ -384,8 +395,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
     if (active) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int xk = tb + r * NB, xj = ta;
-        if (N % R != 0 && xk >= N) break;
+        const int xb = tb + r * NB;
+        if (N % R != 0 && xb >= N) break;
+        const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
         const Real* bb = ch.b + cid * N3 + (xk * N + xj) * N;
 #pragma unroll
         for (int i = 0; i < N; i += 2) bpre[r][i / 2] = __ldg(reinterpret_cast<const V2*>(bb + i));
@@ -403,8 +415,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
     const bool slot_m = inb_m || wrap, slot_p = inb_p || wrap;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int xk = tb + r * NB, xj = ta;
-      if (N % R != 0 && xk >= N) break;
+      const int xb = tb + r * NB;
+      if (N % R != 0 && xb >= N) break;
+      const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
       Real bl[N], cl[N];
 #pragma unroll
       for (int i = 0; i < N; ++i) {
@@ -431,8 +444,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
     if (active) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int xk = tb + r * NB, xj = ta;
-        if (N % R != 0 && xk >= N) break;
+        const int xb = tb + r * NB;
+        if (N % R != 0 && xb >= N) break;
+        const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
         Real* out = y + cid * N3 + (xk * N + xj) * N;
         if constexpr (N % 2 == 0) {
 #pragma unroll
@@ -451,8 +465,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
     if (active) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int xk = tb + r * NB, xj = ta;
-        if (N % R != 0 && xk >= N) break;
+        const int xb = tb + r * NB;
+        if (N % R != 0 && xb >= N) break;
+        const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
 #pragma unroll
         for (int i = 0; i < N; ++i) O[at(LOUT, i, xj, xk)] = res[r][i];
       }
@@ -473,8 +488,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
     if (active) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int xk = tb + r * NB, xj = ta;
-        if (N % R != 0 && xk >= N) break;
+        const int xb = tb + r * NB;
+        if (N % R != 0 && xb >= N) break;
+        const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
         const Real* bb = ch.b + cid * N3 + (xk * N + xj) * N;
         if constexpr (kPreB) {
 #pragma unroll
@@ -496,8 +512,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       if (active) {   // x: T^{-T} -> R2 (x-write / y-read)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int xk = tb + r * NB, xj = ta;
-          if (N % R != 0 && xk >= N) break;
+          const int xb = tb + r * NB;
+          if (N % R != 0 && xb >= N) break;
+          const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
           Real o[N];
           pinv_pre<N, MODE>(kp, res[r], o);
           Real* W = R2 + cslot * LYX.CS;
@@ -563,8 +580,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       if (active) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int xk = tb + r * NB, xj = ta;
-          if (N % R != 0 && xk >= N) break;
+          const int xb = tb + r * NB;
+          if (N % R != 0 && xb >= N) break;
+          const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
           const int64_t gb = cid * N3 + (xk * N + xj) * N;
 #pragma unroll
           for (int i = 0; i < N; i += 2) {
@@ -592,8 +610,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       if (active) {   // x: T^{-1}, three-term update (Eq. (11)) along the x-lines
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int xk = tb + r * NB, xj = ta;
-          if (N % R != 0 && xk >= N) break;
+          const int xb = tb + r * NB;
+          if (N % R != 0 && xb >= N) break;
+          const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
           const Real* Rd = R1 + cslot * LYX.CS;
           Real v[N], z[N];
 #pragma unroll
@@ -624,8 +643,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       if (active) {   // x: T^{-T}
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int xk = tb + r * NB, xj = ta;
-          if (N % R != 0 && xk >= N) break;
+          const int xb = tb + r * NB;
+          if (N % R != 0 && xb >= N) break;
+          const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
           Real o[N];
           pinv_pre<N, MODE>(kp, res[r], o);
 #pragma unroll
@@ -699,8 +719,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       if (active) {   // x: T^{-1}
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int xk = tb + r * NB, xj = ta;
-          if (N % R != 0 && xk >= N) break;
+          const int xb = tb + r * NB;
+          if (N % R != 0 && xb >= N) break;
+          const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
           Real v[N], o[N];
 #pragma unroll
           for (int i = 0; i < N; ++i) v[i] = Y2[at(LYX, i, xj, xk)];
@@ -736,8 +757,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       if (active) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int xk = tb + r * NB, xj = ta;
-          if (N % R != 0 && xk >= N) break;
+          const int xb = tb + r * NB;
+          if (N % R != 0 && xb >= N) break;
+          const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
           const Real* dv = ch.dinv + cid * N3 + (xk * N + xj) * N;
 #pragma unroll
           for (int i = 0; i < N; ++i) X1[at(LXZ, i, xj, xk)] = res[r][i] * __ldg(dv + i);
@@ -782,7 +804,7 @@ cudaError_t launch_t(const KronParamsT<Real>& kp, const GridArgs& g, const Real*
   if (planes <= 0 || g.Nx <= 0 || g.Ny <= 0) return cudaSuccess;
   if (g.Ny > 65535 || planes > 65535) return cudaErrorInvalidValue;
   const dim3 grid((g.Nx + Lay::CPB - 1) / Lay::CPB, g.Ny, planes);
-  const dim3 block(N, Lay::NB * Lay::CPB);
+  const dim3 block = Lay::TPCP == Lay::TPC ? dim3(N, Lay::NB * Lay::CPB) : dim3(Lay::CPB * Lay::TPCP);
   const size_t smem = (size_t)Lay::doubles() * sizeof(Real);
   auto kern = k_kron4<N, NL, MODE, OUTD, ALT, Real>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -798,7 +820,7 @@ cudaError_t launch_mode(int mode, const KronParamsT<Real>& kp, const GridArgs& g
     const char* e = std::getenv("DG_K4_OUT");
     return e ? std::atoi(e) : (N % 2 == 0 ? 1 : 0);   // measured: direct wins for even n only
   }();
-  static const int alt = [] {   // DG_K4_ALT=1: the two-lines-per-thread configuration (n = 6, 8)
+  static const int alt = [] {   // DG_K4_ALT=1: the alternate configuration (n = 5, 6, 8)
     const char* e = std::getenv("DG_K4_ALT");
     return e ? std::atoi(e) : 0;
   }();
