@@ -1,0 +1,37 @@
+"""The opt-in kernel variants (selected by environment variables the library reads once per
+process) against the oracle, each in its own subprocess (tests/_variant_check.py): the
+previous x-first Cartesian kernel, the k_quad general kernel, the n = 5/6/8 alternates of
+k_kron4, the other output path of k_kron4, the z-first basis change at every degree and the
+L2-prefetch settings.  The defaults are covered by test_gpu_parity.py."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+VARIANTS = [
+    ({"DG_KRON": "3"}, "2,5", False),
+    ({"DG_QUAD": "1"}, "3", True),
+    ({"DG_K4_ALT": "1"}, "4,5,7", False),
+    ({"DG_K4_OUT": "0"}, "3,5", False),
+    ({"DG_K4_OUT": "1"}, "2,4", False),
+    ({"DG_BCHG": "4"}, "1,3,4,5,6,7", False),
+    ({"DG_BCHG": "1"}, "2,8", False),
+    ({"DG_L2PF": "0"}, "5", False),
+    ({"DG_L2PF": "2"}, "4", False),
+]
+
+
+@pytest.mark.parametrize("env,degrees,curved", VARIANTS,
+                         ids=[",".join(f"{k}={v}" for k, v in e.items()) for e, _, _ in VARIANTS])
+def test_variant_parity(env, degrees, curved):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cmd = [sys.executable, os.path.join(HERE, "_variant_check.py"), degrees] + (["curved"] if curved else [])
+    r = subprocess.run(cmd, env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
