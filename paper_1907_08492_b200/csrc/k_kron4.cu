@@ -45,6 +45,10 @@ struct Lay3 {
   int Pj, Pk, CS;
 };
 
+#ifndef K4_PREB_ODD
+#define K4_PREB_ODD 1   // odd-n Chebyshev b preload: 0 none, 1 after the Y->X barrier, 2 before it
+#endif
+
 // Per n: lines per thread R, cells per block CPB, and the field layouts
 // addr = i + j*Pj + k*Pk + cell*CS chosen by tools/smem_layout_search6.py (half-warp model)
 // (ZY: z-write/y-read, YX: y-write/x-read, XZ: x-write/z-read).
@@ -384,7 +388,26 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       }
     }
   }
+  // Chebyshev, n = 3, 7: scalar x-line loads of b issued ahead of the residual (measured
+  // +3% / +0.4% at p = 2 / 6; n = 5 has no registers to spare, n = 9 spills: -0.8%)
+  constexpr bool kPreBs = K4_PREB_ODD != 0 && MODE != KMODE_APPLY && (N == 3 || N == 7);
+  Real bso[kPreBs ? R : 1][kPreBs ? N : 1];
+  auto load_bso = [&]() {
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int xb = tb + r * NB;
+        if (N % R != 0 && xb >= N) break;
+        const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
+        const Real* bb = ch.b + cid * N3 + (xk * N + xj) * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) bso[r][i] = __ldg(bb + i);
+      }
+    }
+  };
+  if constexpr (kPreBs && K4_PREB_ODD == 2) load_bso();
   __syncthreads();
+  if constexpr (kPreBs && K4_PREB_ODD == 1) load_bso();
 
   // ================================================================ X
   Real res[R][N];
@@ -499,6 +522,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
             res[r][i] = bv.x - res[r][i];
             res[r][i + 1] = bv.y - res[r][i + 1];
           }
+        } else if constexpr (kPreBs) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) res[r][i] = bso[r][i] - res[r][i];
         } else {
 #pragma unroll
           for (int i = 0; i < N; ++i) res[r][i] = __ldg(bb + i) - res[r][i];
