@@ -157,8 +157,9 @@ dg_status dg_apply_laplace(dg_mesh m, const double* u, double* y, int32_t flags,
 dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, void* stream);
 
 /* y_host = A u_host with HOST vectors (n_local_dofs each): the host->device copy, the matvec
- * and the device->host copy run in z-plane chunks overlapped on internal copy streams (the
- * chunk being computed needs the first plane of the next one).  Stream-ordered on `stream`:
+ * and the device->host copy run in z-plane chunks (min(32, nz/2); env DG_HOST_CHUNKS caps it)
+ * overlapped on internal copy streams (the chunk being computed needs the first plane of the
+ * next one).  Stream-ordered on `stream`:
  * y_host is complete when `stream` reaches the end of the call.  Pinned host memory is needed
  * for the overlap (pageable memory works, copied synchronously by the driver).  Periodic z,
  * several slabs or fewer than 4 planes use one whole-vector copy each way.  The library keeps

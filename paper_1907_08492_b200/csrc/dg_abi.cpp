@@ -1345,7 +1345,11 @@ dg_status dg_apply_laplace_host(dg_mesh m, const double* u_host, double* y_host,
     return DG_OK;
   }
   const int64_t plane = (int64_t)m->N[0] * m->N[1] * m->n * m->n * m->n;
-  const int nchunk = std::min(8, m->nz / 2);
+  // z-plane chunks: the first chunk's copy-in and the last chunk's copy-out are not overlapped,
+  // so more chunks hide more of the PCIe time (DG_HOST_CHUNKS overrides the cap)
+  const char* hc = std::getenv("DG_HOST_CHUNKS");
+  const int cap = hc ? std::max(1, std::atoi(hc)) : 32;
+  const int nchunk = std::max(1, std::min(cap, m->nz / 2));
   while ((int)m->ev_h2d.size() < nchunk) {
     cudaEvent_t a, b;
     CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));

@@ -267,10 +267,18 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
     }
   };
   // next plane's tile (same x-run and row) into L2: its block runs about one wave later
+  // DG_L2PF=3: also pull this block's own tiles of the later Chebyshev streams into L2 now,
+  // so that their loads (b in X, dinv and u_{j-1} in the P^{-1} stages) hit L2
+  if (MODE != KMODE_APPLY && g.l2pf == 3) {
+    const int64_t off = (rowcell + cx0) * N3, cnt = (int64_t)ncell * N3;
+    l2_prefetch(ch.b + off, cnt, btid, BT);
+    if (ch.dinv) l2_prefetch(ch.dinv + off, cnt, btid, BT);
+    if (!ch.first) l2_prefetch(ch.u_prev + off, cnt, btid, BT);
+  }
   if (g.l2pf && cz + 1 < g.zend) {
     const int64_t off = (rowcell + plane + cx0) * N3, cnt = (int64_t)ncell * N3;
     l2_prefetch(u + off, cnt, btid, BT);
-    if (MODE != KMODE_APPLY && g.l2pf > 1) {
+    if (MODE != KMODE_APPLY && g.l2pf == 2) {
       l2_prefetch(ch.b + off, cnt, btid, BT);
       if (ch.dinv) l2_prefetch(ch.dinv + off, cnt, btid, BT);
       if (!ch.first) l2_prefetch(ch.u_prev + off, cnt, btid, BT);

@@ -24,6 +24,7 @@ VARIANTS = [
     ({"DG_BCHG": "1"}, "2,8", False),
     ({"DG_L2PF": "0"}, "5", False),
     ({"DG_L2PF": "2"}, "4", False),
+    ({"DG_L2PF": "3"}, "3,6", False),
 ]
 
 
