@@ -275,9 +275,11 @@ GridArgs grid_args(dg_mesh m, int zbeg, int zend) {
   g.halo_hi = m->d_recv_hi;
   static const int l2pf = [] {
     const char* e = std::getenv("DG_L2PF");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : -1;
   }();
-  g.l2pf = l2pf;
+  // default: next plane's u tile; at n = 3 also the own Chebyshev tiles (measured +4-5% for
+  // the p = 2 Chebyshev step, neutral elsewhere)
+  g.l2pf = l2pf >= 0 ? l2pf : (m->n == 3 ? 3 : 1);
   return g;
 }
 
