@@ -157,7 +157,8 @@ dg_status dg_apply_laplace(dg_mesh m, const double* u, double* y, int32_t flags,
 dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, void* stream);
 
 /* y_host = A u_host with HOST vectors (n_local_dofs each): the host->device copy, the matvec
- * and the device->host copy run in z-plane chunks (min(32, nz/2); env DG_HOST_CHUNKS caps it)
+ * and the device->host copy run in z-plane chunks (up to 32 of >= 4 MB, at most nz/2; env
+ * DG_HOST_CHUNKS sets the cap)
  * overlapped on internal copy streams (the chunk being computed needs the first plane of the
  * next one).  Stream-ordered on `stream`:
  * y_host is complete when `stream` reaches the end of the call.  Pinned host memory is needed

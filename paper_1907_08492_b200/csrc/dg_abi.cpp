@@ -1350,7 +1350,9 @@ dg_status dg_apply_laplace_host(dg_mesh m, const double* u_host, double* y_host,
   // z-plane chunks: the first chunk's copy-in and the last chunk's copy-out are not overlapped,
   // so more chunks hide more of the PCIe time (DG_HOST_CHUNKS overrides the cap)
   const char* hc = std::getenv("DG_HOST_CHUNKS");
-  const int cap = hc ? std::max(1, std::atoi(hc)) : 32;
+  // default: up to 32 chunks of at least 4 MB (small meshes lose more to per-chunk overhead)
+  const int cap = hc ? std::max(1, std::atoi(hc))
+                     : (int)std::min<int64_t>(32, std::max<int64_t>(1, nd * 8 / (4 << 20)));
   const int nchunk = std::max(1, std::min(cap, m->nz / 2));
   while ((int)m->ev_h2d.size() < nchunk) {
     cudaEvent_t a, b;
