@@ -26,7 +26,7 @@ VARIANTS = [
     ({"DG_L2PF": "2"}, "4", False),
     ({"DG_L2PF": "3"}, "3,6", False),
     ({"DG_K5": "1"}, "3,5,7", False),
-    ({"DG_K5": "1", "DG_K5_ZC": "3"}, "3", False),
+    ({"DG_K5": "1", "DG_K5_ZC": "2"}, "3,7", False),
 ]
 
 
