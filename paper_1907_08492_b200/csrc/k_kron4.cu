@@ -1026,8 +1026,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
+#ifndef K5_MIN_BLOCKS
+#define K5_MIN_BLOCKS 2   // measured: 3 blocks/SM spills 128-416 B and runs 1.2-1.6x slower
+#endif
 template <int N>
-__global__ void __launch_bounds__(K4Layout<N, 2>::CPB * K4Layout<N, 2>::TPC, (k4_min_blocks<N, 2, 0, double, KMODE_APPLY>()))
+__global__ void __launch_bounds__(K4Layout<N, 2>::CPB * K4Layout<N, 2>::TPC, K5_MIN_BLOCKS)
 k_kron5(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g, const double* __restrict__ u,
         double* __restrict__ y, int zc) {
   using Real = double;
@@ -1038,7 +1041,7 @@ k_kron5(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
   constexpr Lay3 LZY = Lay::ZY, LYX = Lay::YX;
   constexpr int PG = Lay::PG, GPG = Lay::GPG, GFS = Lay::GFS;
   static_assert(N % 2 == 0, "k_kron5: even n (16-byte aligned cell tiles)");
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   Real* R1 = reinterpret_cast<Real*>(smem_raw);
   Real* R2 = R1 + CPB * Lay::S1;
   Real* GYb = R2 + CPB * Lay::S2;
