@@ -1126,8 +1126,9 @@ k_kron5(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs 
     const bool carried = cz > z0;
     // plane cz+2 into L2 now: its layers 0..NL-1 are the z+ ghosts of the next plane, and the
     // y-neighbour blocks read their ghost z-lines of plane cz+1 from the tiles prefetched here
-    if (g.l2pf && cz + 2 < g.zend) l2_prefetch(u + (rowcell + 2 * plane + cx0) * N3, (int64_t)ncell * N3, btid, BT);
-    else if (g.l2pf && cz == z0 && cz + 1 < g.zend) l2_prefetch(u + (rowcell + plane + cx0) * N3, (int64_t)ncell * N3, btid, BT);
+    // (only planes of this block's chunk: a plane beyond it is read much later by another block)
+    if (g.l2pf && cz + 2 < z1) l2_prefetch(u + (rowcell + 2 * plane + cx0) * N3, (int64_t)ncell * N3, btid, BT);
+    else if (g.l2pf && cz == z0 && cz + 1 < z1) l2_prefetch(u + (rowcell + plane + cx0) * N3, (int64_t)ncell * N3, btid, BT);
     auto job_target = [&](int job, const Real*& src, Real*& dst, int& ds) {
       if (job < nyj) {
         const int c = job / NYJ, jj = job - c * NYJ;
