@@ -16,7 +16,12 @@ Modules
              (Eqs. (11), (12)).
 
 Parity status: every function is pinned by tests under tests/test_oracle_*.py
-against paper-printed values, closed forms or independent constructions, except
-the curved-face penalty convention (mean of A_F/V_K of both sides), which the
-paper does not fix: "parity unpinned" (SURVEY.md §8(c) reading 5).
+against paper-printed values, closed forms or independent constructions.  The
+non-Cartesian geometry (the J^{-T} metric of Eq. (3), normals and areas of Eq. (1))
+is pinned by tests/test_oracle_brute.py: a 40-digit mpmath face-wise bilinear form
+with a numerically differentiated map, SIPG consistency of a mapped bubble on affine
+bricks, and the single-cell energy identity that fixes the curved-face penalty to the
+documented mean of A_F/V_K of both sides (SURVEY.md §8(c) reading 5; R5 —
+the paper does not choose mean vs max, the pin holds the oracle to the documented
+choice).  tools/oracle_mutants.py shows those pins fail for eight plausible mistakes.
 """
