@@ -18,6 +18,10 @@
  *         ((cz_local*Ny + cy)*Nx + cx) * n^3 + (k*n + j)*n + i,   n = degree+1,
  *     x fastest inside a cell and across cells, z slowest (a z-slab of a rank
  *     is one contiguous range).
+ *   - Every vector pointer passed to a call must be 16-byte aligned (the kernels
+ *     move even-n lines with 128-bit accesses); a misaligned pointer returns
+ *     DG_ERR_PARAM before any launch.  cudaMalloc / torch allocations are; a
+ *     view at an odd element offset is not.
  *   - Calls are stream-ordered and asynchronous on the given cudaStream_t
  *     (passed as void*; NULL = legacy default stream).  Asynchronous CUDA/NCCL
  *     faults surface on a later call, or immediately with DG_DEBUG_SYNC=1.
@@ -91,8 +95,21 @@ typedef struct {
   int32_t geometry;        /* DG_GEOM_*; CONSTANT/PER_CELL require deform_amp == 0          */
   int32_t bc[3];           /* DG_BC_* per direction                                         */
   double  penalty_factor;  /* multiplies (p+1)^2 A_F/V_K; <= 0 means 1.0 (paper value)       */
-  const double* user_inv_jac; /* optional HOST array, PER_CELL only: 9 doubles per OWNED cell,
-                              row-major J^{-1}, cell order as the DoF layout; NULL = derive */
+  const double* user_inv_jac; /* optional HOST array, PER_CELL only: exactly 9 doubles per OWNED
+                              cell (9 * Nx * Ny * nz_local; the library reads that many and
+                              cannot check the length), row-major J^{-1}, cell order as the
+                              DoF layout; NULL = derive                                    */
+  const double* user_penalty; /* optional HOST array of sigma_F, 6 doubles per OWNED cell in face
+                              order 2d+s (face xi_d = s of the cell), cell order as the DoF
+                              layout; the value is sigma_F itself (penalty_factor is not
+                              applied).  The two cells of every face inside the slab (also
+                              across a periodic wrap) must carry bit-equal values, else
+                              DG_ERR_PARAM; non-finite or negative values -> DG_ERR_PARAM.
+                              NULL = (p+1)^2 pf mean(A_F/V_K).  A mesh with
+                              user penalties runs the general quadrature kernels (geometry
+                              stored per quadrature point, or per cell for PER_CELL), never
+                              the Cartesian Kronecker, FDM or fp32 paths, whose 1D blocks
+                              assume one penalty per direction.                            */
   int32_t rank, nranks;    /* z-slab decomposition: rank r owns planes
                               [r*Nz/nranks, (r+1)*Nz/nranks)                                */
   const void* nccl_unique_id; /* 128 bytes from dg_get_nccl_unique_id on rank 0, broadcast

@@ -18,8 +18,11 @@ neighbour for u+), (p+1)^3 Gauss points in the cell and (p+1)^2 on each face
   mirror Dirichlet u+ = -u-, grad u+ = grad u- (reading 4),
   periodic: the neighbour wraps,
   sigma_F = (p+1)^2 * penalty_factor * (A_F/V_K- + A_F/V_K+)/2, A_F and V_K by the
-  same Gauss rules; boundary faces use A_F/V_K- (reading 5 —
-  the curved-mesh mean is PARITY UNPINNED, the Cartesian value (p+1)^2/h is pinned).
+  same Gauss rules; boundary faces use A_F/V_K- (reading 5, pinned
+  by tests/test_oracle_brute.py: the Cartesian value (p+1)^2/h, and the documented
+  mean on curved interior faces through the single-cell energy identity),
+  or, when `user_penalty` (ncells, 6) is given, sigma_F = user_penalty[K, 2d+s]
+  (the caller's per-face penalty; equal on both sides of a face).
 The neighbour's gradient uses the neighbour's own Jacobian at the shared point.
 
 Dense tables Phi[q][j] = phi_j(xi_q) over all 3D points and functions are library
@@ -41,8 +44,10 @@ def _tensor_table(rows, deriv_dir=None, drows=None):
 
 
 class SIPG:
-    def __init__(self, mesh: Mesh, p: int, basis: str = "hermite", penalty_factor: float = 1.0):
+    def __init__(self, mesh: Mesh, p: int, basis: str = "hermite", penalty_factor: float = 1.0,
+                 user_penalty=None):
         self.mesh, self.p, self.basis, self.pf = mesh, p, basis, penalty_factor
+        self.user_penalty = None if user_penalty is None else np.asarray(user_penalty, np.float64).reshape(-1, 6)
         n = self.n = p + 1
         t = basis1d.tables(p, basis)
         self.t = t
@@ -168,6 +173,8 @@ class SIPG:
                 AFp = dAp.sum(1)
                 sig_int = 0.5 * (AF / V + AFp / Vp)
                 sig = (p + 1) ** 2 * self.pf * np.where(mirror, AF / V, sig_int)
+                if self.user_penalty is not None:
+                    sig = self.user_penalty[cells, 2 * d + s]
                 jump = um - up                                      # (C,F,R)
                 avg = 0.5 * np.einsum("cfm,cfmr->cfr", nvec, gm + gp)
                 rv = dA[..., None] * (sig[:, None, None] * jump - avg)

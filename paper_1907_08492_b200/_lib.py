@@ -23,6 +23,7 @@ class DgDesc(ctypes.Structure):
         ("bc", ctypes.c_int32 * 3),
         ("penalty_factor", ctypes.c_double),
         ("user_inv_jac", ctypes.POINTER(ctypes.c_double)),
+        ("user_penalty", ctypes.POINTER(ctypes.c_double)),
         ("rank", ctypes.c_int32),
         ("nranks", ctypes.c_int32),
         ("nccl_unique_id", ctypes.c_void_p),

@@ -52,6 +52,8 @@ def _ptr(t, n=None, name="tensor", dtype=None):
         raise ValueError(f"{name} must be contiguous")
     if n is not None and t.numel() < n:
         raise ValueError(f"{name} has {t.numel()} elements, need {n}")
+    if t.data_ptr() % 16:
+        raise ValueError(f"{name} must be 16-byte aligned (dg.h conventions); got a view at an odd offset")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -120,7 +122,8 @@ class Mesh:
     def __init__(self, degree, n_cells, basis="hermite", box_lo=(0.0, 0.0, 0.0),
                  box_hi=(1.0, 1.0, 1.0), linear_map=None, deform_amp=0.0, geometry="constant",
                  bc=("dirichlet", "dirichlet", "dirichlet"), penalty_factor=1.0,
-                 user_inv_jac=None, rank=0, nranks=1, nccl_unique_id=None, stream=None):
+                 user_inv_jac=None, user_penalty=None, rank=0, nranks=1, nccl_unique_id=None,
+                 stream=None):
         L = lib()
         d = DgDesc()
         d.degree = int(degree)
@@ -140,8 +143,20 @@ class Mesh:
         if user_inv_jac is not None:
             import numpy as np
             arr = np.ascontiguousarray(user_inv_jac, dtype=np.float64).reshape(-1)
+            nloc = int(n_cells[0]) * int(n_cells[1]) * self._local_planes(n_cells[2], rank, nranks)
+            if arr.size != 9 * nloc:
+                raise ValueError(f"user_inv_jac has {arr.size} doubles, need 9 per owned cell = {9 * nloc}")
             self._jac_keepalive = arr
             d.user_inv_jac = arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        self._pen_keepalive = None
+        if user_penalty is not None:
+            import numpy as np
+            arr = np.ascontiguousarray(user_penalty, dtype=np.float64).reshape(-1)
+            nloc = int(n_cells[0]) * int(n_cells[1]) * self._local_planes(n_cells[2], rank, nranks)
+            if arr.size != 6 * nloc:
+                raise ValueError(f"user_penalty has {arr.size} doubles, need 6 per owned cell = {6 * nloc}")
+            self._pen_keepalive = arr
+            d.user_penalty = arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         d.rank = int(rank)
         d.nranks = int(nranks)
         self._id_keepalive = None
@@ -160,6 +175,12 @@ class Mesh:
         self.z_begin, self.z_end = zb.value, ze.value
         self.degree = int(degree)
         self.n = self.degree + 1
+
+    @staticmethod
+    def _local_planes(Nz, rank, nranks):
+        P = max(int(nranks), 1)
+        r = int(rank)
+        return (r + 1) * int(Nz) // P - r * int(Nz) // P
 
     # ------------------------------------------------------------------ lifetime
     def close(self):

@@ -31,6 +31,17 @@ dg_status fail(dg_status s, const char* fmt, ...) {
   return s;
 }
 
+// Vector arguments: the kernels use 128-bit accesses (double2 / float4 lines for even n),
+// so every caller vector must be 16-byte aligned (dg.h "Conventions"); a misaligned
+// pointer is rejected here instead of faulting (and poisoning the context) in a kernel.
+bool misaligned(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15u) != 0; }
+
+#define CHECK_ALIGNED(ptr)                                                          \
+  do {                                                                              \
+    if (misaligned(ptr))                                                            \
+      return fail(DG_ERR_PARAM, "%s = %p is not 16-byte aligned", #ptr, (const void*)(ptr)); \
+  } while (0)
+
 bool debug_sync() {
   static int v = -1;
   if (v < 0) {
@@ -197,6 +208,8 @@ struct dg_mesh_s {
   double* d_G = nullptr;          // PER_QPOINT cell tensors
   double* d_face[3] = {nullptr, nullptr, nullptr};
   double* d_jinv = nullptr;       // PER_CELL J^-1 + det J (with ghost planes)
+  double* d_usig[3] = {nullptr, nullptr, nullptr};   // user sigma_F per face (dg.h user_penalty)
+  bool user_pen = false;
   int zlo = ZSRC_MIRROR, zhi = ZSRC_MIRROR;
   // lazily built inverse diagonals
   double* d_dinv_gl = nullptr;
@@ -344,6 +357,54 @@ dg_status halo_exchange_impl(dg_mesh m, const double* u, cudaStream_t s);
 dg_status run_pass(dg_mesh m, int mode, bool kron, const double* u, double* y, const ChebyArgs& ch,
                    bool halo_ready, cudaStream_t s);
 
+// Per-face penalties from the caller's per-cell array (dg.h user_penalty):
+// sig[d][fid] in the face layout of the geometry arrays (x: [z][y][Nx+1], y: [z][Ny+1][x],
+// z: [nz+1][y][x]; local planes).  The face between lower cell (plane pl-1, face 2d+1) and
+// upper cell (plane pl, face 2d) takes their common value; both present and different ->
+// DG_ERR_PARAM.  z faces of a slab boundary with a remote peer take the owned side.
+dg_status build_user_sigma(const double* up, const int N[3], int nz, int bc[3], bool zwrap,
+                           std::vector<double> sig[3]) {
+  const int Nx = N[0], Ny = N[1];
+  const int64_t plane = (int64_t)Nx * Ny;
+  const int64_t ncl = plane * nz;
+  for (int64_t c = 0; c < ncl * 6; ++c)
+    if (!(up[c] >= 0.0) || !std::isfinite(up[c]))
+      return fail(DG_ERR_PARAM, "user_penalty[%lld] = %g is negative or not finite", (long long)c, up[c]);
+  const int nloc[3] = {Nx, Ny, nz};
+  for (int d = 0; d < 3; ++d) {
+    const int nf[3] = {Nx + (d == 0), Ny + (d == 1), nz + (d == 2)};
+    const bool per = d < 2 ? bc[d] == DG_BC_PERIODIC : zwrap;
+    sig[d].assign((size_t)nf[0] * nf[1] * nf[2], 0.0);
+    for (int fz = 0; fz < nf[2]; ++fz)
+      for (int fy = 0; fy < nf[1]; ++fy)
+        for (int fx = 0; fx < nf[0]; ++fx) {
+          const int64_t fid = ((int64_t)fz * nf[1] + fy) * nf[0] + fx;
+          int c[3] = {fx, fy, fz};
+          const int pl = c[d], Nd = nloc[d];
+          double vals[2];
+          int nv = 0;
+          int lo = pl - 1, hi = pl;
+          if (lo < 0) lo = per ? Nd - 1 : -1;
+          if (hi >= Nd) hi = per ? 0 : -1;
+          if (lo >= 0) {
+            int cc[3] = {c[0], c[1], c[2]};
+            cc[d] = lo;
+            vals[nv++] = up[(((int64_t)cc[2] * Ny + cc[1]) * Nx + cc[0]) * 6 + 2 * d + 1];
+          }
+          if (hi >= 0) {
+            int cc[3] = {c[0], c[1], c[2]};
+            cc[d] = hi;
+            vals[nv++] = up[(((int64_t)cc[2] * Ny + cc[1]) * Nx + cc[0]) * 6 + 2 * d];
+          }
+          if (nv == 2 && vals[0] != vals[1])
+            return fail(DG_ERR_PARAM, "user_penalty differs on the two sides of face (d=%d, %d,%d,%d): %g vs %g",
+                        d, fx, fy, fz, vals[0], vals[1]);
+          sig[d][fid] = nv ? vals[0] : 0.0;
+        }
+  }
+  return DG_OK;
+}
+
 // z-slab partition and peers (shared by dg_slab_plan and dg_mesh_setup)
 void slab_plan(int Nz, int P, int r, int bcz, int out[4]) {
   out[0] = (int)((int64_t)r * Nz / P);
@@ -393,6 +454,7 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
   dg_mesh m = new dg_mesh_s();
   m->desc = *d;
   m->desc.user_inv_jac = nullptr;
+  m->desc.user_penalty = nullptr;
   m->rank = d->rank;
   m->nranks = nranks;
   if (!build_tables(d->degree, d->basis, d->penalty_factor, &m->tab)) {
@@ -431,6 +493,13 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
   for (int k = 0; k < 3; ++k) m->h[k] = (d->box_hi[k] - d->box_lo[k]) / m->N[k];
   m->geom = d->geometry == DG_GEOM_PER_QPOINT ? GEOM_PER_QPOINT
             : (d->geometry == DG_GEOM_PER_CELL ? GEOM_PER_CELL : GEOM_CONST);
+  if (d->user_penalty) {
+    // per-face penalties: the general kernels with per-face data (constant geometry is
+    // stored per quadrature point so the penalty can ride in the face arrays)
+    m->user_pen = true;
+    m->cartesian = false;
+    if (m->geom == GEOM_CONST) m->geom = GEOM_PER_QPOINT;
+  }
   if (d->geometry != DG_GEOM_PER_CELL && d->user_inv_jac) {
     delete m;
     return fail(DG_ERR_PARAM, "user_inv_jac requires DG_GEOM_PER_CELL");
@@ -606,7 +675,28 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
       return fail(DG_ERR_CUDA, "per-cell geometry: %s", cudaGetErrorString(e1));
     }
     m->ga.jinv = m->d_jinv;
-  } else if (m->geom == GEOM_PER_QPOINT) {
+  }
+  std::vector<double> usig[3];
+  if (m->user_pen) {
+    int bcv[3] = {d->bc[0], d->bc[1], d->bc[2]};
+    dg_status st = build_user_sigma(d->user_penalty, m->N, m->nz, bcv, m->zlo == ZSRC_LOCAL, usig);
+    if (st != DG_OK) {
+      dg_mesh_destroy(m);
+      return st;
+    }
+    for (int k = 0; k < 3; ++k) {
+      cudaError_t e1 = cudaMalloc(&m->d_usig[k], sizeof(double) * std::max<size_t>(usig[k].size(), 1));
+      if (e1 == cudaSuccess)
+        e1 = cudaMemcpy(m->d_usig[k], usig[k].data(), sizeof(double) * usig[k].size(), cudaMemcpyHostToDevice);
+      if (e1 != cudaSuccess) {
+        dg_mesh_destroy(m);
+        return fail(DG_ERR_CUDA, "user penalty upload: %s", cudaGetErrorString(e1));
+      }
+    }
+    if (m->geom == GEOM_PER_CELL)
+      for (int k = 0; k < 3; ++k) m->ga.sig[k] = m->d_usig[k];
+  }
+  if (m->geom == GEOM_PER_QPOINT) {
     const int64_t n3 = (int64_t)n * n * n;
     MapParams mp{};
     for (int k = 0; k < 9; ++k) mp.L[k] = L[k];
@@ -630,7 +720,8 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
       e1 = cudaMalloc(&m->d_face[k], sizeof(double) * fcount[k] * 4 * n * n);
     if (e1 == cudaSuccess) e1 = cudaMalloc(&d_err, sizeof(int));
     if (e1 == cudaSuccess) e1 = cudaMemsetAsync(d_err, 0, sizeof(int), s);
-    if (e1 == cudaSuccess) e1 = launch_geom_qpoint(n, mp, Nx, Ny, nz, m->d_G, m->d_face, d_err, s);
+    const double* const us[3] = {m->d_usig[0], m->d_usig[1], m->d_usig[2]};
+    if (e1 == cudaSuccess) e1 = launch_geom_qpoint(n, mp, Nx, Ny, nz, m->d_G, m->d_face, us, d_err, s);
     int herr = 0;
     if (e1 == cudaSuccess) e1 = cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
     if (e1 == cudaSuccess) e1 = cudaStreamSynchronize(s);
@@ -661,6 +752,7 @@ dg_status dg_mesh_destroy(dg_mesh m) {
   cudaFree(m->d_G);
   for (int d = 0; d < 3; ++d) cudaFree(m->d_face[d]);
   cudaFree(m->d_jinv);
+  for (int d = 0; d < 3; ++d) cudaFree(m->d_usig[d]);
   cudaFree(m->d_dinv_gl);
   cudaFree(m->d_dinv_pj);
   cudaFree(m->d_dot);
@@ -773,11 +865,14 @@ dg_status dg_tables_1d(int32_t degree, int32_t basis, double pf, double* out, in
 
 dg_status dg_halo_exchange(dg_mesh m, const double* u, void* stream) {
   if (!m || !u) return fail(DG_ERR_PARAM, "NULL argument");
+  CHECK_ALIGNED(u);
   return halo_exchange_impl(m, u, (cudaStream_t)stream);
 }
 
 dg_status dg_apply_laplace(dg_mesh m, const double* u, double* y, int32_t flags, void* stream) {
   if (!m || !u || !y) return fail(DG_ERR_PARAM, "NULL argument");
+  CHECK_ALIGNED(u);
+  CHECK_ALIGNED(y);
   if (u == y) return fail(DG_ERR_PARAM, "u and y alias");
   if (flags & ~(DG_APPLY_HALO_READY | DG_APPLY_QUADRATURE)) return fail(DG_ERR_PARAM, "bad flags");
   cudaStream_t s = (cudaStream_t)stream;
@@ -788,6 +883,8 @@ dg_status dg_apply_laplace(dg_mesh m, const double* u, double* y, int32_t flags,
 
 dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, void* stream) {
   if (!m || !in || !out) return fail(DG_ERR_PARAM, "NULL argument");
+  CHECK_ALIGNED(in);
+  CHECK_ALIGNED(out);
   const int n = m->n;
   const Tables1D& t = m->tab;
   double B[kMaxN * kMaxN];
@@ -816,6 +913,7 @@ dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, 
 
 dg_status dg_inverse_diagonal(dg_mesh m, int32_t inner, double* out, void* stream) {
   if (!m || !out) return fail(DG_ERR_PARAM, "NULL argument");
+  CHECK_ALIGNED(out);
   cudaStream_t s = (cudaStream_t)stream;
   const bool gl = inner == DG_INNER_GL_JACOBI;
   if (!gl && inner != DG_INNER_POINT_JACOBI) return fail(DG_ERR_PARAM, "bad inner %d", inner);
@@ -831,6 +929,9 @@ dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* wor
                               double lambda_max, double lo_frac, double hi_frac, int32_t inner,
                               void* stream) {
   if (!m || !b || !x || !work2) return fail(DG_ERR_PARAM, "NULL argument");
+  CHECK_ALIGNED(b);
+  CHECK_ALIGNED(x);
+  CHECK_ALIGNED(work2);
   if (degree < 0) return fail(DG_ERR_PARAM, "degree < 0");
   const double alpha = lo_frac * lambda_max, beta = hi_frac * lambda_max;
   if (!(alpha > 0 && beta > alpha) || !std::isfinite(beta))
@@ -1054,6 +1155,8 @@ extern "C" {
 
 dg_status dg_apply_preconditioner(dg_mesh m, int32_t inner, const double* r, double* z, void* stream) {
   if (!m || !r || !z) return fail(DG_ERR_PARAM, "NULL argument");
+  CHECK_ALIGNED(r);
+  CHECK_ALIGNED(z);
   if (inner != DG_INNER_GL_JACOBI && inner != DG_INNER_POINT_JACOBI && inner != DG_INNER_FDM)
     return fail(DG_ERR_PARAM, "bad inner %d", inner);
   return pinv_impl(m, inner, r, z, (cudaStream_t)stream);
@@ -1061,6 +1164,8 @@ dg_status dg_apply_preconditioner(dg_mesh m, int32_t inner, const double* r, dou
 
 dg_status dg_dot(dg_mesh m, const double* a, const double* b, double* out, void* stream) {
   if (!m || !a || !b || !out) return fail(DG_ERR_PARAM, "NULL argument");
+  CHECK_ALIGNED(a);
+  CHECK_ALIGNED(b);
   return dot_impl(m, a, b, out, (cudaStream_t)stream);
 }
 
@@ -1118,6 +1223,8 @@ dg_status dg_pcg(dg_mesh m, const double* b, double* x, double rel_tol, int32_t 
                  double lambda_max, double lo_frac, double hi_frac, int32_t inner, int32_t* iters, double* rel_res,
                  void* stream) {
   if (!m || !b || !x) return fail(DG_ERR_PARAM, "NULL argument");
+  CHECK_ALIGNED(b);
+  CHECK_ALIGNED(x);
   if (max_iter < 0 || cheby_degree < 1) return fail(DG_ERR_PARAM, "max_iter < 0 or cheby_degree < 1");
   if (b == x) return fail(DG_ERR_PARAM, "b and x must not alias");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1206,6 +1313,8 @@ extern "C" {
 
 dg_status dg_apply_laplace_f32(dg_mesh m, const float* u, float* y, void* stream) {
   if (!m || !u || !y) return fail(DG_ERR_PARAM, "NULL argument");
+  CHECK_ALIGNED(u);
+  CHECK_ALIGNED(y);
   if (u == y) return fail(DG_ERR_PARAM, "u and y must not alias");
   dg_status st = f32_check(m);
   if (st != DG_OK) return st;
@@ -1219,6 +1328,9 @@ dg_status dg_chebyshev_smooth_f32(dg_mesh m, const float* b, float* x, float* wo
                                   double lambda_max, double lo_frac, double hi_frac, int32_t inner,
                                   void* stream) {
   if (!m || !b || !x || !work2) return fail(DG_ERR_PARAM, "NULL argument");
+  CHECK_ALIGNED(b);
+  CHECK_ALIGNED(x);
+  CHECK_ALIGNED(work2);
   if (degree < 0) return fail(DG_ERR_PARAM, "degree < 0");
   const double alpha = lo_frac * lambda_max, beta = hi_frac * lambda_max;
   if (!(alpha > 0 && beta > alpha) || !std::isfinite(beta))

@@ -97,6 +97,7 @@ struct GeomArgs {
   const double* face[3];       // PER_QPOINT: per direction [face][4][n^2]: dA J^-1 n_+ (3), sigma dA
   const double* jinv;          // PER_CELL:  [cell][10]: J^-1 (row-major), det J
   double pen;                  // (p+1)^2 * penalty_factor  (PER_CELL)
+  const double* sig[3];        // PER_CELL with user penalties: sigma_F per face, layout of face[d]
 };
 
 // Analytic mesh map: x = L X + amp s(Xh), X = lo + (c+xi) h.
@@ -157,8 +158,10 @@ cudaError_t launch_d2f(const double* in, float* out, int64_t n, cudaStream_t s);
 cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* part, double* out, cudaStream_t s);
 cudaError_t launch_axpby(double alpha, const double* x, double beta, double* y, int64_t n, cudaStream_t s);
 cudaError_t launch_lanczos_start(double* v, int64_t n, int64_t g0, cudaStream_t s);
+// usig[d] (may be NULL): the caller's sigma_F per face (dg.h user_penalty) replacing the
+// computed mean; face layout of face[d]
 cudaError_t launch_geom_qpoint(int n, const MapParams& mp, int Nx, int Ny, int nz, double* G,
-                               double* face[3], int* err_flag, cudaStream_t s);
+                               double* face[3], const double* const usig[3], int* err_flag, cudaStream_t s);
 // diagonal of the operator in a basis given by tables (S, DS, v0, v1, d0, d1 at the
 // Gauss points), any geometry; invert -> 1/diag
 struct DiagTables {

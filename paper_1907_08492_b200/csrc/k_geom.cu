@@ -113,7 +113,7 @@ __global__ void k_geom_cells(const MapParams mp, int Nx, int Ny, int nz, double*
 
 template <int N>
 __global__ void k_geom_faces(const MapParams mp, int d, int Nx, int Ny, int nz, const double* V,
-                             double* F, int* err) {
+                             const double* __restrict__ usig, double* F, int* err) {
   constexpr int NN = N * N;
   const int nfx = d == 0 ? Nx + 1 : Nx, nfy = d == 1 ? Ny + 1 : Ny, nfz = d == 2 ? nz + 1 : nz;
   const int64_t total = (int64_t)nfx * nfy * nfz;
@@ -178,20 +178,21 @@ __global__ void k_geom_faces(const MapParams mp, int d, int Nx, int Ny, int nz, 
       sig = mp.pen * AF / vol(0);
     else
       sig = mp.pen * AF / vol(-1);
+    if (usig) sig = usig[t];   // the caller's sigma_F (dg.h user_penalty), same face layout
     for (int p = 0; p < NN; ++p) out[3 * NN + p] *= sig;
   }
 }
 
 template <int N>
-cudaError_t run(const MapParams& mp, int Nx, int Ny, int nz, double* G, double* face[3], int* err,
-                cudaStream_t s) {
+cudaError_t run(const MapParams& mp, int Nx, int Ny, int nz, double* G, double* face[3],
+                const double* const usig[3], int* err, cudaStream_t s) {
   double* V = nullptr;
   cudaError_t e = cudaMallocAsync(&V, sizeof(double) * (size_t)Nx * Ny * (nz + 2), s);
   if (e != cudaSuccess) return e;
   const int grid = 148 * 8, bs = 256;
   k_volumes<N><<<grid, bs, 0, s>>>(mp, Nx, Ny, nz, V);
   k_geom_cells<N><<<grid, bs, 0, s>>>(mp, Nx, Ny, nz, G, err);
-  for (int d = 0; d < 3; ++d) k_geom_faces<N><<<grid, bs, 0, s>>>(mp, d, Nx, Ny, nz, V, face[d], err);
+  for (int d = 0; d < 3; ++d) k_geom_faces<N><<<grid, bs, 0, s>>>(mp, d, Nx, Ny, nz, V, usig[d], face[d], err);
   e = cudaGetLastError();
   cudaFreeAsync(V, s);
   return e;
@@ -200,16 +201,16 @@ cudaError_t run(const MapParams& mp, int Nx, int Ny, int nz, double* G, double* 
 }  // namespace
 
 cudaError_t launch_geom_qpoint(int n, const MapParams& mp, int Nx, int Ny, int nz, double* G,
-                               double* face[3], int* err_flag, cudaStream_t s) {
+                               double* face[3], const double* const usig[3], int* err_flag, cudaStream_t s) {
   switch (n) {
-    case 2: return run<2>(mp, Nx, Ny, nz, G, face, err_flag, s);
-    case 3: return run<3>(mp, Nx, Ny, nz, G, face, err_flag, s);
-    case 4: return run<4>(mp, Nx, Ny, nz, G, face, err_flag, s);
-    case 5: return run<5>(mp, Nx, Ny, nz, G, face, err_flag, s);
-    case 6: return run<6>(mp, Nx, Ny, nz, G, face, err_flag, s);
-    case 7: return run<7>(mp, Nx, Ny, nz, G, face, err_flag, s);
-    case 8: return run<8>(mp, Nx, Ny, nz, G, face, err_flag, s);
-    case 9: return run<9>(mp, Nx, Ny, nz, G, face, err_flag, s);
+    case 2: return run<2>(mp, Nx, Ny, nz, G, face, usig, err_flag, s);
+    case 3: return run<3>(mp, Nx, Ny, nz, G, face, usig, err_flag, s);
+    case 4: return run<4>(mp, Nx, Ny, nz, G, face, usig, err_flag, s);
+    case 5: return run<5>(mp, Nx, Ny, nz, G, face, usig, err_flag, s);
+    case 6: return run<6>(mp, Nx, Ny, nz, G, face, usig, err_flag, s);
+    case 7: return run<7>(mp, Nx, Ny, nz, G, face, usig, err_flag, s);
+    case 8: return run<8>(mp, Nx, Ny, nz, G, face, usig, err_flag, s);
+    case 9: return run<9>(mp, Nx, Ny, nz, G, face, usig, err_flag, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -87,6 +87,10 @@ __device__ __forceinline__ void face_geom(const QuadParams& qp, const GeomArgs& 
 #pragma unroll
     for (int k = 0; k < 3; ++k) ckm[k] = fac * (Ji[k * 3] * r[0] + Ji[k * 3 + 1] * r[1] + Ji[k * 3 + 2] * r[2]);
     double sig;
+    int64_t fid;   // face index in the layout of the per-face arrays (user penalties)
+    if (d == 0) fid = ((int64_t)czl * g.Ny + cy) * (g.Nx + 1) + cx + s;
+    else if (d == 1) fid = ((int64_t)czl * (g.Ny + 1) + cy + s) * g.Nx + cx;
+    else fid = ((int64_t)(czl + s) * g.Ny + cy) * g.Nx + cx;
     if (mirror) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) ckp[k] = ckm[k];
@@ -108,6 +112,7 @@ __device__ __forceinline__ void face_geom(const QuadParams& qp, const GeomArgs& 
       const double nrp = sqrt(rp[0] * rp[0] + rp[1] * rp[1] + rp[2] * rp[2]);
       sig = ga.pen * 0.5 * (nr + nrp);
     }
+    if (ga.sig[d]) sig = __ldg(ga.sig[d] + fid);   // dg.h user_penalty: sigma_F as given
     sdA = sig * detJ * nr * ww;
     (void)cid;
   }

@@ -53,3 +53,15 @@ def test_host_tables_match_oracle(p, basis):
         T, Ti = basis1d.change_matrix(p)
         np.testing.assert_allclose(np.asarray(t["T"]).reshape(T.shape), T, rtol=2e-16, atol=1e-28)
         np.testing.assert_allclose(np.asarray(t["Tinv"]).reshape(Ti.shape), Ti, rtol=1e-15, atol=1e-15)
+
+
+def test_binding_checks_host_array_lengths():
+    """The library reads 9 (user_inv_jac) / 6 (user_penalty) doubles per owned cell from raw
+    host pointers and cannot check the length; the binding does, before dg_mesh_setup."""
+    import paper_1907_08492_b200 as P
+    with pytest.raises(ValueError, match="user_inv_jac"):
+        P.Mesh(degree=2, n_cells=(2, 2, 2), geometry="per_cell", user_inv_jac=np.ones(9 * 8 - 1))
+    with pytest.raises(ValueError, match="user_penalty"):
+        P.Mesh(degree=2, n_cells=(2, 2, 3), user_penalty=np.ones(6 * 12 + 6))
+    with pytest.raises(ValueError, match="user_penalty"):   # rank 1 of 2 owns planes [1, 3)
+        P.Mesh(degree=2, n_cells=(2, 2, 3), user_penalty=np.ones(6 * 4), rank=1, nranks=2)
