@@ -162,6 +162,29 @@ dg_status dg_mesh_query_halo(dg_mesh m, int64_t* count, int32_t* lo_peer, int32_
 dg_status dg_halo_pack(dg_mesh m, const double* u, double* send_lo, double* send_hi, void* stream);
 dg_status dg_halo_set(dg_mesh m, const double* recv_lo, const double* recv_hi, void* stream);
 
+/* Caller-provided transport for a mesh built with nranks > 1 and nccl_unique_id == NULL
+ * (external mode), so that the calls which need an exchange inside them -- the fused
+ * Chebyshev sweep (one halo per step), dg_dot, dg_lanczos_lambda_max, dg_pcg and
+ * dg_apply_laplace without DG_APPLY_HALO_READY -- run over any transport (MPI, a Python
+ * process group, or the one-GPU loopback of the tests).
+ *   halo:  called after the library packed the send planes of the current operand on
+ *          `stream` (device buffers, `count` doubles each; send_lo / recv_lo are NULL when
+ *          there is no lower peer, likewise for hi).  It must leave recv_lo / recv_hi (the
+ *          library-owned halo) holding the peers' planes when work enqueued on `stream`
+ *          after the return runs (synchronous copies, or copies ordered on `stream`).
+ *          Message order as dg_slab_plan: the lower peer's top planes go to recv_lo, the
+ *          upper peer's bottom planes to recv_hi.
+ *   allreduce_sum: replace *value (host) by its sum over all ranks.
+ * Both return 0 on success; non-zero becomes DG_ERR_NCCL ("transport failed").
+ * Passing NULL removes the transport.  The callbacks run on the calling thread. */
+typedef struct {
+  int (*halo)(void* user, const double* send_lo, const double* send_hi, double* recv_lo,
+              double* recv_hi, int64_t count, void* stream);
+  int (*allreduce_sum)(void* user, double* value);
+  void* user;
+} dg_transport;
+dg_status dg_set_transport(dg_mesh m, const dg_transport* t);
+
 /* Fill the library-owned z-halo of u: the two Hermite face layers (all n layers for
  * the GL basis) of the neighbouring ranks' boundary planes, via grouped ncclSend/
  * ncclRecv.  No-op when nranks == 1 and no periodic wrap in z. */
@@ -195,8 +218,9 @@ dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* wor
 
 /* ---------------------------------------------------------------- solver layer
  * (PAPER.md:1811-1832).  All vectors are device, n_local_dofs
- * long; dot products are global over the z-slabs (ncclAllReduce when nranks > 1; the
- * external-transport mode returns DG_ERR_UNSUPPORTED).  These calls synchronise `stream`. */
+ * long; dot products are global over the z-slabs (ncclAllReduce when nranks > 1, the
+ * dg_transport's allreduce_sum in external mode, DG_ERR_UNSUPPORTED in external mode
+ * without a transport).  These calls synchronise `stream`. */
 
 /* z = P^{-1} r, the inner preconditioner of dg_chebyshev_smooth (DG_INNER_*). */
 dg_status dg_apply_preconditioner(dg_mesh m, int32_t inner, const double* r, double* z, void* stream);

@@ -31,7 +31,17 @@ class DgDesc(ctypes.Structure):
     ]
 
 
+HALO_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double))
+
+
+class DgTransport(ctypes.Structure):
+    _fields_ = [("halo", HALO_FN), ("allreduce_sum", ALLREDUCE_FN), ("user", ctypes.c_void_p)]
+
+
 SYMBOLS = {
+    "dg_set_transport": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(DgTransport)]),
     # name: (restype, argtypes)
     "dg_last_error": (ctypes.c_char_p, []),
     "dg_version": (ctypes.c_char_p, []),

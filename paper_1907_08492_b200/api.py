@@ -8,7 +8,7 @@ import ctypes
 
 import torch
 
-from ._lib import DgDesc, lib
+from ._lib import ALLREDUCE_FN, HALO_FN, DgDesc, DgTransport, lib
 
 DG_OK = 0
 STATUS = {0: "DG_OK", 1: "DG_ERR_PARAM", 2: "DG_ERR_NUMERIC", 3: "DG_ERR_CUDA",
@@ -228,6 +228,43 @@ class Mesh:
         lo = _ptr(recv_lo, cnt, "recv_lo") if recv_lo is not None else ctypes.c_void_p(0)
         hi = _ptr(recv_hi, cnt, "recv_hi") if recv_hi is not None else ctypes.c_void_p(0)
         _check(lib().dg_halo_set(self._h, lo, hi, _stream(stream)), "dg_halo_set")
+
+    def set_transport(self, halo, allreduce_sum):
+        """dg_set_transport (external mode): halo(send_lo, send_hi, recv_lo, recv_hi, count, stream)
+        gets raw device pointers (int or None) and must fill the recv planes; allreduce_sum(x)
+        returns the sum of the host float x over all ranks.  Exceptions become a non-zero
+        status (DG_ERR_NCCL "transport failed").  halo=None removes the transport."""
+        if halo is None:
+            _check(lib().dg_set_transport(self._h, None), "dg_set_transport")
+            self._transport = None
+            return
+
+        def _halo(user, slo, shi, rlo, rhi, count, stream):
+            try:
+                halo(slo, shi, rlo, rhi, int(count), stream)
+                return 0
+            except Exception:                      # noqa: BLE001 - reported as a status
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        def _sum(user, val):
+            try:
+                val[0] = float(allreduce_sum(float(val[0])))
+                return 0
+            except Exception:                      # noqa: BLE001
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        t = DgTransport(HALO_FN(_halo), ALLREDUCE_FN(_sum), None)
+        self._transport = t                        # keeps the C callbacks alive
+        _check(lib().dg_set_transport(self._h, ctypes.byref(t)), "dg_set_transport")
+
+    def halo_set_raw(self, recv_lo_ptr, recv_hi_ptr, stream=None):
+        """dg_halo_set with raw device pointers (for transports)."""
+        _check(lib().dg_halo_set(self._h, ctypes.c_void_p(recv_lo_ptr or 0), ctypes.c_void_p(recv_hi_ptr or 0),
+                                 _stream(stream)), "dg_halo_set")
 
     def apply_laplace(self, u, y=None, flags=0, stream=None):
         if y is None:

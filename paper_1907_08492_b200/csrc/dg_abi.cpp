@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -222,6 +224,8 @@ struct dg_mesh_s {
   int64_t halo_count = 0;         // doubles per halo buffer
   ncclComm_t comm = nullptr;
   bool external = false;          // nranks > 1 without NCCL: dg_halo_pack / dg_halo_set
+  dg_transport transport{};       // external mode: caller's halo / all-reduce callbacks
+  std::string comm_key;           // NCCL unique id bytes of the shared communicator
   int lo_peer = -1, hi_peer = -1;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
@@ -403,6 +407,47 @@ dg_status build_user_sigma(const double* up, const int N[3], int nz, int bc[3], 
         }
   }
   return DG_OK;
+}
+
+// NCCL communicators shared by every mesh built from the same unique id (one
+// ncclCommInitRank per id and rank; e.g. the per-degree meshes of the bench), refcounted.
+struct CommEntry {
+  ncclComm_t comm;
+  int refs;
+};
+std::mutex g_comm_mu;
+std::map<std::string, CommEntry> g_comms;
+
+ncclResult_t comm_acquire(const void* id128, int nranks, int rank, ncclComm_t* out, std::string* key) {
+  std::lock_guard<std::mutex> lk(g_comm_mu);
+  std::string k(reinterpret_cast<const char*>(id128), 128);
+  k += std::to_string(nranks) + ":" + std::to_string(rank);
+  auto it = g_comms.find(k);
+  if (it != g_comms.end()) {
+    it->second.refs++;
+    *out = it->second.comm;
+    *key = k;
+    return ncclSuccess;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclComm_t c = nullptr;
+  ncclResult_t r = ncclCommInitRank(&c, nranks, id, rank);
+  if (r != ncclSuccess) return r;
+  g_comms[k] = CommEntry{c, 1};
+  *out = c;
+  *key = k;
+  return ncclSuccess;
+}
+
+void comm_release(const std::string& key) {
+  std::lock_guard<std::mutex> lk(g_comm_mu);
+  auto it = g_comms.find(key);
+  if (it == g_comms.end()) return;
+  if (--it->second.refs == 0) {
+    ncclCommDestroy(it->second.comm);
+    g_comms.erase(it);
+  }
 }
 
 // z-slab partition and peers (shared by dg_slab_plan and dg_mesh_setup)
@@ -617,9 +662,7 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
     cudaMemsetAsync(m->d_recv_lo, 0, bytes, s);
     cudaMemsetAsync(m->d_recv_hi, 0, bytes, s);
     if (d->nccl_unique_id) {
-      ncclUniqueId id;
-      std::memcpy(&id, d->nccl_unique_id, sizeof id);
-      ncclResult_t r = ncclCommInitRank(&m->comm, nranks, id, d->rank);
+      ncclResult_t r = comm_acquire(d->nccl_unique_id, nranks, d->rank, &m->comm, &m->comm_key);
       if (r != ncclSuccess) {
         m->comm = nullptr;
         dg_mesh_destroy(m);
@@ -769,7 +812,7 @@ dg_status dg_mesh_destroy(dg_mesh m) {
   cudaFree(m->d_recv_hi);
   cudaFree(m->d_send_lo);
   cudaFree(m->d_send_hi);
-  if (m->comm) ncclCommDestroy(m->comm);
+  if (m->comm) comm_release(m->comm_key);
   if (m->ev_ready) cudaEventDestroy(m->ev_ready);
   if (m->ev_halo) cudaEventDestroy(m->ev_halo);
   if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
@@ -860,6 +903,14 @@ dg_status dg_tables_1d(int32_t degree, int32_t basis, double pf, double* out, in
   put(t.v0, n); put(t.v1, n); put(t.d0, n); put(t.d1, n);
   put(t.Mhat, n * n); put(t.Ahat, n * n); put(t.Lhat, n * n); put(t.Nm, n * n); put(t.Np, n * n);
   put(t.T, n * n); put(t.Tinv, n * n);
+  return DG_OK;
+}
+
+dg_status dg_set_transport(dg_mesh m, const dg_transport* t) {
+  if (!m) return fail(DG_ERR_PARAM, "NULL mesh");
+  if (t && (!t->halo || !t->allreduce_sum)) return fail(DG_ERR_PARAM, "dg_transport needs both callbacks");
+  if (t && !m->external) return fail(DG_ERR_PARAM, "dg_set_transport: mesh is not in external-transport mode");
+  m->transport = t ? *t : dg_transport{};
   return DG_OK;
 }
 
@@ -1005,10 +1056,22 @@ namespace {
 
 dg_status halo_exchange_impl(dg_mesh m, const double* u, cudaStream_t s) {
   if (m->zlo != ZSRC_HALO && m->zhi != ZSRC_HALO) return DG_OK;
-  if (m->external)
+  if (m->external && !m->transport.halo)
     return fail(DG_ERR_UNSUPPORTED, "external halo transport: call dg_halo_pack/dg_halo_set and "
-                                    "DG_APPLY_HALO_READY");
+                                    "DG_APPLY_HALO_READY, or install a dg_transport");
   const int64_t plane_cells = (int64_t)m->N[0] * m->N[1];
+  if (m->external) {   // caller's transport: pack here, the callback fills recv_lo / recv_hi
+    cudaError_t e = launch_halo_pack(u, m->lo_peer >= 0 ? m->d_send_lo : nullptr,
+                                     m->hi_peer >= 0 ? m->d_send_hi : nullptr, m->n, m->NL, plane_cells,
+                                     m->nz, s);
+    if (e != cudaSuccess) return fail(DG_ERR_CUDA, "halo pack: %s", cudaGetErrorString(e));
+    m->launches++;
+    const bool lo = m->lo_peer >= 0, hi = m->hi_peer >= 0;
+    if (m->transport.halo(m->transport.user, lo ? m->d_send_lo : nullptr, hi ? m->d_send_hi : nullptr,
+                          lo ? m->d_recv_lo : nullptr, hi ? m->d_recv_hi : nullptr, m->halo_count, s) != 0)
+      return fail(DG_ERR_NCCL, "transport failed (halo callback returned non-zero)");
+    return DG_OK;
+  }
   cudaError_t e = launch_halo_pack(u, m->lo_peer >= 0 ? m->d_send_lo : nullptr,
                                    m->hi_peer >= 0 ? m->d_send_hi : nullptr, m->n, m->NL, plane_cells,
                                    m->nz, s);
@@ -1048,7 +1111,11 @@ dg_status run_pass(dg_mesh m, int mode, bool kron, const double* u, double* y, c
   };
   const bool need = (m->zlo == ZSRC_HALO || m->zhi == ZSRC_HALO) && !halo_ready;
   if (!need) return launch(0, m->nz);
-  if (m->external) return halo_exchange_impl(m, u, s);   // reports the error
+  if (m->external) {   // caller's transport: exchange first, then every plane
+    dg_status st = halo_exchange_impl(m, u, s);
+    if (st != DG_OK) return st;
+    return launch(0, m->nz);
+  }
   CUDA_TRY(cudaEventRecord(m->ev_ready, s));
   CUDA_TRY(cudaStreamWaitEvent(m->comm_stream, m->ev_ready, 0));
   dg_status st = halo_exchange_impl(m, u, m->comm_stream);
@@ -1094,11 +1161,16 @@ dg_status dot_impl(dg_mesh m, const double* a, const double* b, double* out, cud
   if (st != DG_OK) return st;
   m->launches++;   // two kernels
   if (m->nranks > 1) {
-    if (!m->comm) return fail(DG_ERR_UNSUPPORTED, "global dot products need the NCCL communicator");
-    NCCL_TRY(ncclAllReduce(res, res, 1, ncclDouble, ncclSum, m->comm, s));
+    if (m->comm) {
+      NCCL_TRY(ncclAllReduce(res, res, 1, ncclDouble, ncclSum, m->comm, s));
+    } else if (!m->transport.allreduce_sum) {
+      return fail(DG_ERR_UNSUPPORTED, "global dot products need the NCCL communicator or a dg_transport");
+    }
   }
   CUDA_TRY(cudaMemcpyAsync(out, res, sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
+  if (m->nranks > 1 && !m->comm && m->transport.allreduce_sum(m->transport.user, out) != 0)
+    return fail(DG_ERR_NCCL, "transport failed (allreduce_sum callback returned non-zero)");
   return DG_OK;
 }
 

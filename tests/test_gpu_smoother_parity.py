@@ -76,6 +76,9 @@ def _pinv_cells(p, inner, dinv_cells, r_cells):
     return sm.basis_change(p, z, "Tinv")
 
 
+_DINV_CACHE = {}
+
+
 @pytest.mark.parametrize("p", range(1, 9))
 @pytest.mark.parametrize("inner", ["gl_jacobi", "point_jacobi"])
 @pytest.mark.parametrize("degree", [1, 2, 5])
@@ -91,9 +94,11 @@ def test_chebyshev_every_degree_multiblock(p, inner, degree):
                     bc=("periodic", "dirichlet", "dirichlet"), seed=900 + p)
     om = mesh_from_spec(spec)
     H = SIPG(om, p)
-    allc = np.arange(om.ncells)
-    dop = SIPG(om, p, "gl") if inner == "gl_jacobi" else H
-    dinv = 1.0 / _diag_by_class(dop, allc)
+    key = (p, inner)
+    if key not in _DINV_CACHE:       # the three sweep degrees share the mesh and its diagonal
+        dop = SIPG(om, p, "gl") if inner == "gl_jacobi" else H
+        _DINV_CACHE[key] = 1.0 / _diag_by_class(dop, np.arange(om.ncells))
+    dinv = _DINV_CACHE[key]
     P = (lambda r: _pinv_cells(p, inner, dinv, r))
     b = uniform_vector(spec.n_dofs, 910 + p)
     x0 = uniform_vector(spec.n_dofs, 920 + p)

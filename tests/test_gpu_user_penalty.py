@@ -28,10 +28,12 @@ def _dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
-def random_face_penalty(spec, rng, lo=5.0, hi=80.0):
+def random_face_penalty(spec, rng, lo=0.8, hi=2.0):
     """(ncells, 6) array: one random sigma per face of the global mesh, copied to both cells
-    of the face (periodic faces wrap), face order 2d+s."""
+    of the face (periodic faces wrap), face order 2d+s; sigma = (p+1)^2 N_d/|box_d| times
+    U(lo, hi), i.e. around the default penalty (well-conditioned, coercive operator)."""
     N = spec.n_cells
+    p = spec.degree
     nc = N[0] * N[1] * N[2]
     out = np.empty((nc, 6))
     for d in range(3):
@@ -39,7 +41,8 @@ def random_face_penalty(spec, rng, lo=5.0, hi=80.0):
         nplanes = N[d] if spec.bc[d] == "periodic" else N[d] + 1
         shape = [N[0], N[1], N[2]]
         shape[d] = nplanes
-        sig = rng.uniform(lo, hi, size=shape[::-1])          # [z][y][x] with plane index along d
+        base = (p + 1) ** 2 * N[d] / (spec.box_hi[d] - spec.box_lo[d])
+        sig = base * rng.uniform(lo, hi, size=shape[::-1])   # [z][y][x] with plane index along d
         for c in range(nc):
             cc = [c % N[0], (c // N[0]) % N[1], c // (N[0] * N[1])]
             for s in (0, 1):
