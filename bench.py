@@ -35,6 +35,8 @@ from synthetic import CONFIGS, c4_spec  # noqa: E402
 
 METRIC = "SIPG Laplace matvec DoF/s (fp64) and achieved HBM GB/s vs peak, p=2..8"
 UNIT = "DoF/s"
+# lambda_max(P^-1 A_H) sanity values (Kronecker + Lanczos, Cartesian, mirror)
+LMAX_SANITY = {2: 2.986, 3: 2.604, 4: 2.500, 5: 2.401, 6: 2.370, 7: 2.402, 8: 2.471}
 BYTES_PER_DOF = {"matvec": 16.0, "basis_change": 16.0, "cheby_first": 32.0, "cheby": 40.0}
 
 
@@ -51,6 +53,7 @@ def args_():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip peaks/e2e/cpu (profiling runs)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C2/C3/C5 and paper-formulation extra keys")
     return ap.parse_args()
 
 
@@ -149,6 +152,47 @@ def cpu_cores_used():
     return 1   # numpy c_einsum loops (the oracle's contractions) run on one thread
 
 
+def _pool_worker(args):
+    """One process of the all-core oracle sample: random cells of a 12^3-cell mesh of the
+    same degree (the oracle's work per cell does not depend on the mesh size)."""
+    p, budget_s, seed = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle.geometry import Mesh
+    from oracle.sipg import SIPG
+    from synthetic import uniform_vector
+    N = 12
+    op = SIPG(Mesh(N=(N, N, N)), p)
+    u = uniform_vector(N ** 3 * (p + 1) ** 3, seed)
+    rng = np.random.default_rng(seed)
+    n3 = (p + 1) ** 3
+    batch = max(1, int(2000 / n3 * 8))
+    done, t_used = 0, 0.0
+    while t_used < budget_s:
+        cells = rng.choice(N ** 3, size=batch, replace=False)
+        t0 = time.perf_counter()
+        op.apply(u, cells=cells)
+        t_used += time.perf_counter() - t0
+        done += batch
+    return done * n3, t_used
+
+
+def oracle_rate_all_cores(degrees, budget_s):
+    """Aggregate oracle matvec DoF/s with one process per host core (os.cpu_count()),
+    each timing `budget_s` of naive quadrature per degree; returns (DoF/s, cores)."""
+    import multiprocessing as mp_
+    cores = os.cpu_count() or 1
+    ctx = mp_.get_context("fork")
+    rates = []
+    with ctx.Pool(cores) as pool:
+        for p in degrees:
+            res = pool.map(_pool_worker, [(p, budget_s, 1000 * p + i) for i in range(cores)])
+            # all processes run concurrently: aggregate rate = sum of per-process rates
+            rates.append((p, sum(d / t for d, t in res)))
+    # sweep rate: total DoF over total time, each degree weighted like the single-core figure
+    inv = sum(1.0 / r for _, r in rates) / len(rates)
+    return 1.0 / inv, cores, {p: r for p, r in rates}
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(a, rank):
     if rank != 0:
@@ -236,6 +280,91 @@ WORKLOAD_TEXT = {
 }
 
 
+OPS_H = {2: 190.7, 3: 218.0, 4: 205.6, 5: 225.3, 6: 223.8, 7: 241.0, 8: 244.0}   # tab:operations opsH,
+# FLOP per DoF of the paper's general-geometry matvec in the Hermite-like basis
+
+
+def make_setups(specs, rank, world, dev, P, torch, nccl_id=None, need_lmax=True):
+    setups = []
+    for spec in specs:
+        p = spec.degree
+        m = P.mesh_from_spec(spec, rank=rank, nranks=world, nccl_unique_id=nccl_id)
+        nl = m.n_local_dofs
+        g = torch.Generator(device=dev)
+        g.manual_seed(spec.seed * 1000 + rank)
+        u = torch.rand(nl, dtype=torch.float64, device=dev, generator=g).mul_(2).sub_(1)
+        g.manual_seed((100 + p) * 1000 + rank)
+        b = torch.rand(nl, dtype=torch.float64, device=dev, generator=g).mul_(2).sub_(1)
+        x = torch.zeros(nl, dtype=torch.float64, device=dev)
+        y = torch.empty_like(u)
+        v = torch.empty_like(u)
+        work2 = torch.empty(2 * nl, dtype=torch.float64, device=dev)
+        lmax = lanczos_lambda_max(m) if need_lmax else None
+        setups.append(dict(p=p, spec=spec, m=m, u=u, b=b, x=x, y=y, v=v, work2=work2, lmax=lmax,
+                           n_global=m.n_global_dofs, key=f"p{p}" + ("-gl" if spec.basis == "gl" else "")
+                           + ("-curved" if spec.deform_amp else "")))
+    torch.cuda.synchronize()
+    return setups
+
+
+def time_steps(setups, a, stream, torch, barrier, ops=("matvec", "basis_change", "cheby"), apply_flags=0):
+    """W warm-up + K timed steps of the listed ops per setup; CUDA events per op on `stream`
+    (each op bracketed by its own events; an L2 flush outside the events when the vectors
+    are smaller than 2x L2).  Returns (per-setup op ms lists, total ms, launches, clocks,
+    l2 flush note)."""
+    dev = setups[0]["u"].device
+    small = min(s["m"].n_local_dofs for s in setups) * 8 < (256 << 20)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if small else None
+
+    def l2_flush():
+        if flush is not None:
+            flush.fill_(1)
+
+    def run_op(s, op):
+        if op == "matvec":
+            s["m"].apply_laplace(s["u"], s["y"], flags=apply_flags)
+        elif op == "basis_change":
+            if s["spec"].basis == "hermite":
+                s["m"].basis_change("T", s["u"], s["v"])
+        else:
+            s["m"].chebyshev_smooth(s["b"], s["x"], s["lmax"], degree=a.cheby_degree, work2=s["work2"])
+
+    def step(record):
+        for s in setups:
+            for op in ops:
+                l2_flush()
+                if record:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                run_op(s, op)
+                if record:
+                    e1.record(stream)
+                    s.setdefault("ev", {}).setdefault(op, []).append((e0, e1))
+
+    for s in setups:
+        s["ev"] = {}
+    for _ in range(a.warmup):
+        step(False)
+    launches0 = sum(s["m"].launch_count for s in setups)
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index or 0) as clk:
+        t_start.record(stream)
+        for _ in range(a.steps):
+            step(True)
+        t_end.record(stream)
+        barrier()
+    launches = sum(s["m"].launch_count for s in setups) - launches0
+    ms = {}
+    for s in setups:
+        ms[s["key"]] = {op: sum(e0.elapsed_time(e1) for e0, e1 in s["ev"][op]) for op in ops}
+    note = ("256 MB buffer overwritten before every timed op (outside its events; vectors < 2x L2)" if small else
+            f"inputs larger than L2 ({min(s['m'].n_local_dofs for s in setups) * 8 / 1e9:.2f} GB or more per "
+            "vector >> 126 MB)")
+    return ms, t_start.elapsed_time(t_end), launches, clk.summary(), note
+
+
 def run_ours(a, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -265,85 +394,19 @@ def run_ours(a, rank, world, local_rank):
     if not a.quick:
         fp64_peak = P.measure_peak("fp64")
     # ---------------------------------------------------------------- setup per degree
-    setups = []
-    for spec in specs:
-        p = spec.degree
-        nccl_id = None
-        if world > 1:
-            obj = [P.get_nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            nccl_id = obj[0]
-        m = P.mesh_from_spec(spec, rank=rank, nranks=world, nccl_unique_id=nccl_id)
-        nl = m.n_local_dofs
-        g = torch.Generator(device=dev)
-        g.manual_seed(spec.seed * 1000 + rank)
-        u = torch.rand(nl, dtype=torch.float64, device=dev, generator=g).mul_(2).sub_(1)
-        g.manual_seed((100 + p) * 1000 + rank)
-        b = torch.rand(nl, dtype=torch.float64, device=dev, generator=g).mul_(2).sub_(1)
-        x = torch.zeros(nl, dtype=torch.float64, device=dev)
-        y = torch.empty_like(u)
-        v = torch.empty_like(u)
-        work2 = torch.empty(2 * nl, dtype=torch.float64, device=dev)
-        lmax = lanczos_lambda_max(m)
-        setups.append(dict(p=p, spec=spec, m=m, u=u, b=b, x=x, y=y, v=v, work2=work2, lmax=lmax,
-                           n_global=m.n_global_dofs, key=f"p{p}" + ("-gl" if spec.basis == "gl" else "")
-                           + ("-curved" if spec.deform_amp else "")))
-    torch.cuda.synchronize()
-    # L2 (126 MB): vectors smaller than 2x L2 (C2: 33 MB) would stay resident between the timed
-    # ops, so then a 256 MB buffer is overwritten before every op, outside its event bracket
-    small = min(s["m"].n_local_dofs for s in setups) * 8 < (256 << 20)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if small else None
-
-    def l2_flush():
-        if flush is not None:
-            flush.fill_(1)
-
-    def step(record):
-        for s in setups:
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if record else None
-            l2_flush()
-            if record:
-                ev[0].record(stream)
-            s["m"].apply_laplace(s["u"], s["y"])
-            if record:
-                ev[1].record(stream)
-            l2_flush()
-            if record:
-                ev[2].record(stream)
-            if s["spec"].basis == "hermite":
-                s["m"].basis_change("T", s["u"], s["v"])
-            if record:
-                ev[3].record(stream)
-            l2_flush()
-            if record:
-                ev[4].record(stream)
-            s["m"].chebyshev_smooth(s["b"], s["x"], s["lmax"], degree=a.cheby_degree, work2=s["work2"])
-            if record:
-                ev[5].record(stream)
-                s.setdefault("events", []).append(ev)
-
-    for _ in range(a.warmup):
-        step(False)
-    launches0 = sum(s["m"].launch_count for s in setups)
-    barrier()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        t_start.record(stream)
-        for _ in range(a.steps):
-            step(True)
-        t_end.record(stream)
-        barrier()
-    launches = sum(s["m"].launch_count for s in setups) - launches0
-    total_ms = allmax(t_start.elapsed_time(t_end))
+    nccl_id = None
+    if world > 1:   # one unique id: every degree's mesh shares one NCCL communicator
+        obj = [P.get_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    setups = make_setups(specs, rank, world, dev, P, torch, nccl_id)
+    op_ms, total_ms, launches, clocks, flush_note = time_steps(setups, a, stream, torch, barrier)
+    total_ms = allmax(total_ms)
     ops = {}
     t_mv_sum = 0.0
     dom = {"matvec": [0.0, 0.0], "basis_change": [0.0, 0.0], "chebyshev_step": [0.0, 0.0]}  # bytes, ms
     for s in setups:
-        mv = sum(e[0].elapsed_time(e[1]) for e in s["events"])
-        bc = sum(e[2].elapsed_time(e[3]) for e in s["events"])
-        ch = sum(e[4].elapsed_time(e[5]) for e in s["events"])
-        mv, bc, ch = allmax(mv), allmax(bc), allmax(ch)
+        mv, bc, ch = (allmax(op_ms[s["key"]][k]) for k in ("matvec", "basis_change", "cheby"))
         t_mv_sum += mv
         nd = s["n_global"]
         K = a.steps
@@ -356,12 +419,16 @@ def run_ours(a, rank, world, local_rank):
             "n_dofs": nd, "lambda_max": s["lmax"],
             "matvec_dofs_per_s": nd * K / (mv * 1e-3),
             "matvec_gbs": mv_bytes * K / (mv * 1e-3) / 1e9,
+            "matvec_frac_hbm": mv_bytes * K / (mv * 1e-3) / 1e9 / world / hbm_peak,
             "matvec_bytes_per_dof": mv_bytes / nd,
             "basis_change_dofs_per_s": nd * K / (bc * 1e-3) if herm else None,
             "basis_change_gbs": nd * BYTES_PER_DOF["basis_change"] * K / (bc * 1e-3) / 1e9 if herm else None,
             "cheby_step_dofs_per_s": nd * cd * K / (ch * 1e-3),
             "cheby_sweep_gbs": ch_bytes * K / (ch * 1e-3) / 1e9,
+            "cheby_frac_hbm": ch_bytes * K / (ch * 1e-3) / 1e9 / world / hbm_peak,
         }
+        if s["spec"].basis == "hermite" and not s["spec"].deform_amp and s["p"] in LMAX_SANITY:
+            ops[s["key"]]["lambda_max_sanity"] = LMAX_SANITY[s["p"]]
         dom["matvec"][0] += mv_bytes * K
         dom["matvec"][1] += mv
         if herm:
@@ -387,6 +454,8 @@ def run_ours(a, rank, world, local_rank):
     roofline = {"bound": "hbm", "kernel": kernel,
                 "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                 "traffic": traffic, "traffic_note": traffic_note, "peak_source": hbm_src,
+                "per_degree_frac": {k: (o["cheby_frac_hbm"] if dom_name == "chebyshev_step" else o["matvec_frac_hbm"])
+                                    for k, o in ops.items()},
                 "note": "achieved = algorithmic bytes (matvec/basis change 16 B/DoF, Chebyshev step "
                         "40 B/DoF, first step 32) / summed CUDA-event time of that op, per GPU"}
     mv_gbs = dom["matvec"][0] / (dom["matvec"][1] * 1e-3) / 1e9 / world
@@ -399,13 +468,32 @@ def run_ours(a, rank, world, local_rank):
             "data": "synthetic: seeded uniform[-1,1) fp64 vectors on Cartesian [0,1]^3 meshes (mirror Dirichlet)",
             "config": {"workload": WORKLOAD_TEXT[a.workload],
                        "degrees": degrees, "n_dofs_total": n_sum,
-                       "l2_flush": ("256 MB buffer overwritten before every timed op (outside its events; "
-                                    "vectors < 2x L2)" if small else
-                                    f"inputs larger than L2 ({min(s['m'].n_local_dofs for s in setups) * 8 / 1e9:.2f}"
-                                    " GB or more per vector >> 126 MB)"),
+                       "l2_flush": flush_note,
                        "parallelism": f"z-slab x{world}"},
             "roofline": roofline, "matvec_roofline": matvec_roof, "ops": ops,
-            "gpu_launches": launches, "clocks": clk.summary()}
+            "gpu_launches": launches, "clocks": clocks}
+
+    # ---------------------------------------------------------------- the paper's formulation on C4
+    # The general quadrature kernel (cell + face quadrature with a constant merged tensor,
+    # PAPER.md:798-804) on the same C4 meshes, matvec only (the paper's benchmark); its roof is
+    # FP64: tab:operations FLOP/DoF x DoF/s vs the measured DFMA peak.
+    if a.workload == "c4" and not a.quick and world == 1 and not a.no_extras:
+        qms, _, _, qclk, _ = time_steps(setups, a, stream, torch, barrier, ops=("matvec",),
+                                        apply_flags=P.APPLY_QUADRATURE)
+        per = {}
+        for s in setups:
+            r = s["n_global"] * a.steps / (qms[s["key"]]["matvec"] * 1e-3)
+            per[s["key"]] = {"matvec_dofs_per_s": r, "flop_per_dof": OPS_H.get(s["p"]),
+                             "tflops": r * OPS_H.get(s["p"], 0) / 1e12,
+                             "frac_fp64": (r * OPS_H.get(s["p"], 0) / 1e12 / fp64_peak) if fp64_peak else None,
+                             "frac_hbm": r * 16 / 1e9 / hbm_peak}
+        line["c4_paper_formulation"] = {
+            "workload": "C4 meshes through the general quadrature kernel k_quad3 (DG_APPLY_QUADRATURE): "
+                        "cell + face quadrature with the constant merged tensor, the paper's benchmark setup",
+            "value": sum(s["n_global"] for s in setups) * a.steps
+            / (sum(qms[s["key"]]["matvec"] for s in setups) * 1e-3),
+            "unit": UNIT, "ops": per, "clocks": qclk,
+            "roof": "fp64: tab:operations opsH FLOP/DoF x DoF/s over dg_measure_peak(fp64)"}
 
     # ---------------------------------------------------------------- FDM smoother (extra)
     # the same fused Chebyshev sweep around the FDM block-Jacobi
@@ -464,33 +552,83 @@ def run_ours(a, rank, world, local_rank):
             uh = torch.empty(nl, dtype=torch.float64, pin_memory=True)
             uh.copy_(s["u"].cpu())
             yh = torch.empty(nl, dtype=torch.float64, pin_memory=True)
-            s["m"].apply_laplace_host(uh, yh, stream=stream)   # warm-up: staging buffers, streams
+            for _ in range(max(1, a.warmup)):   # warm-up: staging buffers, streams
+                s["m"].apply_laplace_host(uh, yh, stream=stream)
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            s["m"].apply_laplace_host(uh, yh, stream=stream)
+            for _ in range(a.steps):
+                s["m"].apply_laplace_host(uh, yh, stream=stream)
             e1.record(stream)
             barrier()
             e2e_ms += allmax(e0.elapsed_time(e1))
             h2d += 8 * s["n_global"]
             d2h += 8 * s["n_global"]
-        line["e2e"] = {"value": n_sum / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            del uh, yh
+        line["e2e"] = {"value": n_sum * a.steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h,
-                       "note": "per degree: dg_apply_laplace_host on pinned host vectors (H2D of u, matvec, D2H "
-                               "of y in overlapped z-plane chunks inside the call); summed over the sweep"}
+                       "note": f"{a.steps} steps of: per degree, dg_apply_laplace_host on pinned host vectors "
+                               "(H2D of u, matvec, D2H of y in overlapped z-plane chunks inside the call); "
+                               "CUDA events around the K steps, summed over the sweep"}
+    # ---------------------------------------------------------------- other BASELINE configs
+    # C3 (curved, per-q-point geometry, k_quad3), C5 (453M DoF, one GPU) and C2 (Hermite vs nodal
+    # GL): the same step (matvec, basis change, degree-5 Chebyshev) with their own clocks; extra
+    # keys, not part of `value`.
+    if a.workload == "c4" and not a.quick and world == 1 and not a.no_extras:
+        del setups
+        torch.cuda.empty_cache()
+        extras = {}
+        for name, specs_x in (("c3", [CONFIGS["C3"]]), ("c5", [CONFIGS["C5"]]),
+                              ("c2", [CONFIGS["C2"], CONFIGS["C2_GL"]])):
+            sx = make_setups(specs_x, 0, 1, dev, P, torch)
+            xms, xtot, xl, xclk, xnote = time_steps(sx, a, stream, torch, barrier)
+            per = {}
+            for s_ in sx:
+                nd, K, cd = s_["n_global"], a.steps, a.cheby_degree
+                gb = geometry_bytes_per_dof(s_["spec"])
+                mv, bc, ch = (xms[s_["key"]][k] for k in ("matvec", "basis_change", "cheby"))
+                mvb = nd * (16.0 + gb)
+                chb = nd * (BYTES_PER_DOF["cheby_first"] + (cd - 1) * BYTES_PER_DOF["cheby"] + cd * gb)
+                herm = s_["spec"].basis == "hermite"
+                per[s_["key"]] = {
+                    "n_dofs": nd, "lambda_max": s_["lmax"], "bytes_per_dof_matvec": mvb / nd,
+                    "matvec_dofs_per_s": nd * K / (mv * 1e-3), "matvec_gbs": mvb * K / (mv * 1e-3) / 1e9,
+                    "matvec_frac_hbm": mvb * K / (mv * 1e-3) / 1e9 / hbm_peak,
+                    "basis_change_gbs": nd * 16.0 * K / (bc * 1e-3) / 1e9 if herm else None,
+                    "cheby_step_dofs_per_s": nd * cd * K / (ch * 1e-3),
+                    "cheby_sweep_gbs": chb * K / (ch * 1e-3) / 1e9,
+                    "cheby_frac_hbm": chb * K / (ch * 1e-3) / 1e9 / hbm_peak}
+            extras[name] = {"workload": WORKLOAD_TEXT[name], "ops": per, "clocks": xclk, "l2_flush": xnote,
+                            "ms_per_step": xtot / a.steps, "gpu_launches": xl}
+            del sx
+            torch.cuda.empty_cache()
+        line["workloads"] = extras
+
     # ---------------------------------------------------------------- CPU oracle baseline
     if rank == 0 and world == 1 and not a.no_cpu_baseline and not a.quick:
         dofs = secs = 0.0
         cells = {}
         for p in sorted(set(degrees)):
-            r, c, t = oracle_rate(p, 3.0)
+            r, c, t = oracle_rate(p, 2.0)
             dofs += r * t
             secs += t
             cells[p] = c
-        line["cpu_baseline"] = {"value": dofs / secs, "unit": UNIT, "cores": cpu_cores_used(),
+        single = dofs / secs
+        try:
+            allc, ncores, per_deg = oracle_rate_all_cores(sorted(set(degrees)), 1.5)
+        except Exception as e:   # noqa: BLE001 - a host without fork keeps the single-core figure
+            allc, ncores, per_deg = None, 1, {"error": str(e)}
+        value_cpu = allc if allc else single
+        line["cpu_baseline"] = {"value": value_cpu, "unit": UNIT, "cores": ncores if allc else 1,
                                 "kind": "oracle",
-                                "sample": f"naive numpy quadrature matvec on random cells of each C4 mesh, "
-                                          f"~3 s per degree; cells {cells}"}
+                                "host_cpu_count": os.cpu_count(),
+                                "single_core_value": single,
+                                "all_core_per_degree": per_deg,
+                                "sample": f"naive numpy quadrature matvec (oracle, untuned). all-core value: one "
+                                          f"process per host core, each ~1.5 s per degree on random cells of a "
+                                          f"12^3-cell mesh of that degree (per-cell work is size-independent); "
+                                          f"single_core_value: one thread, ~2 s per degree on random cells of "
+                                          f"each C4 mesh, cells {cells}; sweep rate = harmonic mean over degrees"}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -504,6 +642,9 @@ def main():
         run_reference(a, rank)
         return
     if world > 1:
+        # NCCL init log (ranks, channels, NVLS) for the scaling runs; INIT subsystem only
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
