@@ -252,6 +252,19 @@ dg_status dg_chebyshev_smooth_f32(dg_mesh m, const float* b, float* x, float* wo
                                   double lambda_max, double lo_frac, double hi_frac, int32_t inner,
                                   void* stream);
 
+/* out = B^{x3} in per cell in single precision (B rounded to float once; in == out allowed);
+ * any geometry (the basis change is cell-local and geometry-free). */
+dg_status dg_basis_change_f32(dg_mesh m, int32_t op, const float* in, float* out, void* stream);
+
+/* Mixed-precision variant of dg_pcg (fp64 CG around a single-precision
+ * preconditioner): CG vectors, matvec and dot products in fp64; every preconditioner
+ * application z = M r rounds r to float, runs the degree-`cheby_degree` Chebyshev sweep
+ * of dg_chebyshev_smooth_f32 from zero and widens z back to double.  Cartesian single-slab
+ * meshes (the fp32 kernels), else DG_ERR_UNSUPPORTED.  Arguments as dg_pcg. */
+dg_status dg_pcg_mixed(dg_mesh m, const double* b, double* x, double rel_tol, int32_t max_iter,
+                       int32_t cheby_degree, double lambda_max, double lo_frac, double hi_frac,
+                       int32_t inner, int32_t* iters, double* rel_res, void* stream);
+
 /* Inverse of the inner preconditioner's diagonal, copied to `out` (device,
  * n_local_dofs): diag(A_GL)^{-1} (GL_JACOBI) or diag(A)^{-1} (POINT_JACOBI). */
 dg_status dg_inverse_diagonal(dg_mesh m, int32_t inner, double* out, void* stream);

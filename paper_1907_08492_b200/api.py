@@ -366,6 +366,28 @@ class Mesh:
                "dg_pcg")
         return it.value, rr.value
 
+    def basis_change_f32(self, op, x, out=None, stream=None):
+        """fp32 basis change B^{x3} per cell (dg_basis_change_f32)."""
+        f32 = torch.float32
+        if out is None:
+            out = torch.empty(self.n_local_dofs, dtype=f32, device="cuda")
+        _check(lib().dg_basis_change_f32(self._h, BCHG[op], _ptr(x, self.n_local_dofs, "in", f32),
+                                         _ptr(out, self.n_local_dofs, "out", f32), _stream(stream)),
+               "dg_basis_change_f32")
+        return out
+
+    def pcg_mixed(self, b, x, lambda_max, rel_tol=1e-9, max_iter=500, cheby_degree=5, lo=0.06, hi=1.2,
+                  inner="gl_jacobi", stream=None):
+        """dg_pcg_mixed: fp64 CG around an fp32 Chebyshev preconditioner.  Returns (iterations,
+        relative residual)."""
+        it = ctypes.c_int32()
+        rr = ctypes.c_double()
+        _check(lib().dg_pcg_mixed(self._h, _ptr(b, self.n_local_dofs, "b"), _ptr(x, self.n_local_dofs, "x"),
+                                  float(rel_tol), int(max_iter), int(cheby_degree), float(lambda_max), float(lo),
+                                  float(hi), INNER[inner], ctypes.byref(it), ctypes.byref(rr), _stream(stream)),
+               "dg_pcg_mixed")
+        return it.value, rr.value
+
     def inverse_diagonal(self, inner="gl_jacobi", out=None, stream=None):
         if out is None:
             out = self.empty()

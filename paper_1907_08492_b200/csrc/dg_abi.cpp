@@ -962,6 +962,28 @@ dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, 
   return post_launch(m, launch_basis_change(n, bp, in, out, m->ncells_local, s), "basis_change", s);
 }
 
+dg_status dg_basis_change_f32(dg_mesh m, int32_t op, const float* in, float* out, void* stream) {
+  if (!m || !in || !out) return fail(DG_ERR_PARAM, "NULL argument");
+  CHECK_ALIGNED(in);
+  CHECK_ALIGNED(out);
+  const int n = m->n;
+  const Tables1D& t = m->tab;
+  double B[kMaxN * kMaxN];
+  switch (op) {
+    case DG_BCHG_H_TO_GL: std::memcpy(B, t.T, sizeof B); break;
+    case DG_BCHG_GL_TO_H: std::memcpy(B, t.Tinv, sizeof B); break;
+    case DG_BCHG_H_TO_GL_T: transpose(t.T, n, B); break;
+    case DG_BCHG_GL_TO_H_T: transpose(t.Tinv, n, B); break;
+    default: return fail(DG_ERR_PARAM, "bad basis-change op %d", op);
+  }
+  BchgParams bp{};
+  pack_eo(B, n, bp.B);
+  BchgParamsF bf{};
+  for (int k = 0; k < kEO; ++k) bf.B[k] = (float)bp.B[k];
+  cudaStream_t s = (cudaStream_t)stream;
+  return post_launch(m, launch_basis_change_f32(n, bf, in, out, m->ncells_local, s), "basis_change_f32", s);
+}
+
 dg_status dg_inverse_diagonal(dg_mesh m, int32_t inner, double* out, void* stream) {
   if (!m || !out) return fail(DG_ERR_PARAM, "NULL argument");
   CHECK_ALIGNED(out);
@@ -1291,15 +1313,25 @@ dg_status dg_lanczos_lambda_max(dg_mesh m, int32_t inner, int32_t iters, double*
   return DG_OK;
 }
 
-dg_status dg_pcg(dg_mesh m, const double* b, double* x, double rel_tol, int32_t max_iter, int32_t cheby_degree,
-                 double lambda_max, double lo_frac, double hi_frac, int32_t inner, int32_t* iters, double* rel_res,
-                 void* stream) {
+}  // extern "C"
+
+namespace {
+
+dg_status f32_check(dg_mesh m);
+
+// CG around the Chebyshev sweep (mixed: the sweep runs in fp32, CG in fp64)
+dg_status pcg_impl(dg_mesh m, const double* b, double* x, double rel_tol, int32_t max_iter, int32_t cheby_degree,
+                   double lambda_max, double lo_frac, double hi_frac, int32_t inner, int32_t* iters,
+                   double* rel_res, cudaStream_t s, bool mixed) {
   if (!m || !b || !x) return fail(DG_ERR_PARAM, "NULL argument");
   CHECK_ALIGNED(b);
   CHECK_ALIGNED(x);
   if (max_iter < 0 || cheby_degree < 1) return fail(DG_ERR_PARAM, "max_iter < 0 or cheby_degree < 1");
   if (b == x) return fail(DG_ERR_PARAM, "b and x must not alias");
-  cudaStream_t s = (cudaStream_t)stream;
+  if (mixed) {
+    dg_status st = f32_check(m);
+    if (st != DG_OK) return st;
+  }
   const int64_t nd = m->ndofs_local;
   DevVecs w;
   for (int i = 0; i < 4; ++i) {
@@ -1311,10 +1343,28 @@ dg_status dg_pcg(dg_mesh m, const double* b, double* x, double rel_tol, int32_t 
   CUDA_TRY(cudaMalloc(&work2, sizeof(double) * (size_t)std::max<int64_t>(2 * nd, 1)));
   w.v.push_back(work2);
   double *r = w.v[0], *z = w.v[1], *p = w.v[2], *q = w.v[3];
+  // fp32 buffers of the mixed variant (r32, z32 and the sweep's two work vectors) in work2's space
+  float* r32 = reinterpret_cast<float*>(work2);
+  float* z32 = r32 + ((nd + 3) & ~int64_t(3));
+  float* w32 = nullptr;
+  if (mixed) {
+    double* tmp = nullptr;
+    CUDA_TRY(cudaMalloc(&tmp, sizeof(double) * (size_t)std::max<int64_t>(nd + 4, 1)));
+    w.v.push_back(tmp);
+    w32 = reinterpret_cast<float*>(tmp);
+  }
   ChebyArgs none{};
   auto precond = [&](const double* rin, double* zout) -> dg_status {   // z = Chebyshev sweep from 0
-    CUDA_TRY(cudaMemsetAsync(zout, 0, sizeof(double) * (size_t)nd, s));
-    return dg_chebyshev_smooth(m, rin, zout, work2, cheby_degree, lambda_max, lo_frac, hi_frac, inner, s);
+    if (!mixed) {
+      CUDA_TRY(cudaMemsetAsync(zout, 0, sizeof(double) * (size_t)nd, s));
+      return dg_chebyshev_smooth(m, rin, zout, work2, cheby_degree, lambda_max, lo_frac, hi_frac, inner, s);
+    }
+    dg_status st = post_launch(m, launch_d2f(rin, r32, nd, s), "d2f", s);
+    if (st != DG_OK) return st;
+    CUDA_TRY(cudaMemsetAsync(z32, 0, sizeof(float) * (size_t)nd, s));
+    st = dg_chebyshev_smooth_f32(m, r32, z32, w32, cheby_degree, lambda_max, lo_frac, hi_frac, inner, s);
+    if (st != DG_OK) return st;
+    return post_launch(m, launch_f2d(z32, zout, nd, s), "f2d", s);
   };
   dg_status st;
   // r = b - A x
@@ -1354,6 +1404,24 @@ dg_status dg_pcg(dg_mesh m, const double* b, double* x, double rel_tol, int32_t 
   if (iters) *iters = k;
   if (rel_res) *rel_res = res;
   return DG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dg_status dg_pcg(dg_mesh m, const double* b, double* x, double rel_tol, int32_t max_iter, int32_t cheby_degree,
+                 double lambda_max, double lo_frac, double hi_frac, int32_t inner, int32_t* iters, double* rel_res,
+                 void* stream) {
+  return pcg_impl(m, b, x, rel_tol, max_iter, cheby_degree, lambda_max, lo_frac, hi_frac, inner, iters, rel_res,
+                  (cudaStream_t)stream, false);
+}
+
+dg_status dg_pcg_mixed(dg_mesh m, const double* b, double* x, double rel_tol, int32_t max_iter,
+                       int32_t cheby_degree, double lambda_max, double lo_frac, double hi_frac, int32_t inner,
+                       int32_t* iters, double* rel_res, void* stream) {
+  return pcg_impl(m, b, x, rel_tol, max_iter, cheby_degree, lambda_max, lo_frac, hi_frac, inner, iters, rel_res,
+                  (cudaStream_t)stream, true);
 }
 
 }  // extern "C"

@@ -68,6 +68,9 @@ using ChebyArgsF = ChebyArgsT<float>;
 struct BchgParams {
   double B[kEO];              // even-odd packed 1D matrix, parity +1
 };
+struct BchgParamsF {
+  float B[kEO];               // BchgParams rounded to float (fp32 path)
+};
 
 // Kernel parameters of the general quadrature path (Eqs. (3)-(5)):
 // 1D tables in even-odd form, face traces restricted to the NL layers next to a
@@ -127,6 +130,8 @@ cudaError_t launch_basis_change4(int n, const BchgParams& bp, const double* in, 
                                  cudaStream_t s);
 cudaError_t launch_basis_change(int n, const BchgParams& bp, const double* in, double* out,
                                 int64_t ncells, cudaStream_t s);
+cudaError_t launch_basis_change_f32(int n, const BchgParamsF& bp, const float* in, float* out,
+                                    int64_t ncells, cudaStream_t s);
 // diagonal of a Cartesian Kronecker operator: d[i,j,k] = sum_d c_d prod(1D diagonals)
 struct CartDiagParams {
   double mdiag[kMaxN];                 // diag(Mhat_basis)
@@ -155,6 +160,7 @@ cudaError_t launch_pinv(int n, int inner, const KronParams& kp, const double* r,
                         int64_t ncells, cudaStream_t s);
 int dot_partials();
 cudaError_t launch_d2f(const double* in, float* out, int64_t n, cudaStream_t s);
+cudaError_t launch_f2d(const float* in, double* out, int64_t n, cudaStream_t s);
 cudaError_t launch_dot(const double* a, const double* b, int64_t n, double* part, double* out, cudaStream_t s);
 cudaError_t launch_axpby(double alpha, const double* x, double beta, double* y, int64_t n, cudaStream_t s);
 cudaError_t launch_lanczos_start(double* v, int64_t n, int64_t g0, cudaStream_t s);

@@ -11,16 +11,16 @@
 namespace dgb {
 namespace {
 
-template <int N, int CPB>
+template <int N, int CPB, typename Real, typename BP>
 __global__ void __launch_bounds__(CPB * N * N)
-k_bchg(const __grid_constant__ BchgParams bp, const double* __restrict__ in,
-       double* __restrict__ out, int64_t ncells) {
+k_bchg(const __grid_constant__ BP bp, const Real* __restrict__ in,
+       Real* __restrict__ out, int64_t ncells) {
   constexpr int P = N | 1, NN = N * N, FIELD = N * N * P;
-  __shared__ double sm[CPB * FIELD];
+  __shared__ Real sm[CPB * FIELD];
   const int64_t cell0 = (int64_t)blockIdx.x * CPB;
   const int ncell = (int)(ncells - cell0 < CPB ? ncells - cell0 : CPB);
   const int tid = threadIdx.x;
-  const double* src = in + cell0 * (N * NN);
+  const Real* src = in + cell0 * (N * NN);
   for (int e = tid; e < ncell * N * NN; e += CPB * NN) {
     const int c = e / (N * NN), r = e % (N * NN);
     sm[c * FIELD + (r / N) * P + r % N] = src[e];
@@ -28,10 +28,10 @@ k_bchg(const __grid_constant__ BchgParams bp, const double* __restrict__ in,
   __syncthreads();
   const int cs = tid / NN, line = tid % NN;
   const bool active = cs < ncell;
-  double* F = sm + cs * FIELD;
+  Real* F = sm + cs * FIELD;
   if (active) {  // x-lines
     const int j = line % N, k = line / N;
-    double x[N], o[N];
+    Real x[N], o[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) x[i] = F[(k * N + j) * P + i];
     eo_apply<N, 1>(bp.B, x, o);
@@ -41,7 +41,7 @@ k_bchg(const __grid_constant__ BchgParams bp, const double* __restrict__ in,
   __syncthreads();
   if (active) {  // y-lines
     const int i = line % N, k = line / N;
-    double x[N], o[N];
+    Real x[N], o[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) x[j] = F[(k * N + j) * P + i];
     eo_apply<N, 1>(bp.B, x, o);
@@ -51,30 +51,27 @@ k_bchg(const __grid_constant__ BchgParams bp, const double* __restrict__ in,
   __syncthreads();
   if (active) {  // z-lines, coalesced store
     const int i = line % N, j = line / N;
-    double x[N], o[N];
+    Real x[N], o[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) x[k] = F[(k * N + j) * P + i];
     eo_apply<N, 1>(bp.B, x, o);
-    double* dst = out + (cell0 + cs) * (N * NN) + j * N + i;
+    Real* dst = out + (cell0 + cs) * (N * NN) + j * N + i;
 #pragma unroll
     for (int k = 0; k < N; ++k) dst[k * NN] = o[k];
   }
 }
 
-template <int N>
-cudaError_t launch_n(const BchgParams& bp, const double* in, double* out, int64_t ncells,
-                     cudaStream_t s) {
+template <int N, typename Real, typename BP>
+cudaError_t launch_n(const BP& bp, const Real* in, Real* out, int64_t ncells, cudaStream_t s) {
   constexpr int CPB = (256 + N * N - 1) / (N * N);
   if (ncells <= 0) return cudaSuccess;
   const int64_t blocks = (ncells + CPB - 1) / CPB;
-  k_bchg<N, CPB><<<(unsigned)blocks, CPB * N * N, 0, s>>>(bp, in, out, ncells);
+  k_bchg<N, CPB, Real, BP><<<(unsigned)blocks, CPB * N * N, 0, s>>>(bp, in, out, ncells);
   return cudaGetLastError();
 }
 
-}  // namespace
-
-cudaError_t launch_basis_change(int n, const BchgParams& bp, const double* in, double* out,
-                                int64_t ncells, cudaStream_t s) {
+template <typename Real, typename BP>
+cudaError_t launch_any(int n, const BP& bp, const Real* in, Real* out, int64_t ncells, cudaStream_t s) {
   switch (n) {
     case 2: return launch_n<2>(bp, in, out, ncells, s);
     case 3: return launch_n<3>(bp, in, out, ncells, s);
@@ -86,6 +83,19 @@ cudaError_t launch_basis_change(int n, const BchgParams& bp, const double* in, d
     case 9: return launch_n<9>(bp, in, out, ncells, s);
   }
   return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+cudaError_t launch_basis_change(int n, const BchgParams& bp, const double* in, double* out,
+                                int64_t ncells, cudaStream_t s) {
+  return launch_any<double>(n, bp, in, out, ncells, s);
+}
+
+// fp32 basis change: the same kernel on floats, B rounded once
+cudaError_t launch_basis_change_f32(int n, const BchgParamsF& bp, const float* in, float* out,
+                                    int64_t ncells, cudaStream_t s) {
+  return launch_any<float>(n, bp, in, out, ncells, s);
 }
 
 }  // namespace dgb

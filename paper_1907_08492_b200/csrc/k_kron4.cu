@@ -47,6 +47,11 @@ struct Lay3 {
   int Pj, Pk, CS;
 };
 
+#ifndef K4_STAGE
+#define K4_STAGE 0      // 1: the Chebyshev streams b, u_{j-1}, dinv of the block's cells are copied to
+                        //    shared memory with cp.async at block start (CPBS cells per block)
+#endif
+
 #ifndef K4_PREB_ODD
 #define K4_PREB_ODD 1   // odd-n Chebyshev b preload: 0 none, 1 after the Y->X barrier, 2 before it
 #endif
@@ -55,20 +60,20 @@ struct Lay3 {
 // addr = i + j*Pj + k*Pk + cell*CS chosen by tools/smem_layout_search6.py (half-warp model)
 // (ZY: z-write/y-read, YX: y-write/x-read, XZ: x-write/z-read).
 template <int N, int ALT = 0> struct K4C;
-template <> struct K4C<3> { static constexpr int R = 1, CPB = 32, TP = 0, XSW = 0; static constexpr Lay3 ZY{3, 19, 57}, YX{3, 9, 27}, XZ{3, 18, 57}; };
-template <> struct K4C<4> { static constexpr int R = 2, CPB = 30, TP = 0, XSW = 0; static constexpr Lay3 ZY{4, 20, 88}, YX{5, 20, 88}, XZ{5, 20, 84}; };
-template <> struct K4C<5> { static constexpr int R = 2, CPB = 16, TP = 0, XSW = 0; static constexpr Lay3 ZY{5, 26, 143}, YX{5, 25, 134}, XZ{5, 25, 139}; };
-template <> struct K4C<6> { static constexpr int R = 1, CPB = 8, TP = 0, XSW = 0; static constexpr Lay3 ZY{6, 38, 228}, YX{9, 54, 324}, XZ{11, 66, 402}; };
-template <> struct K4C<7> { static constexpr int R = 2, CPB = 10, TP = 0, XSW = 0; static constexpr Lay3 ZY{7, 55, 396}, YX{7, 56, 392}, XZ{7, 49, 344}; };
-template <> struct K4C<8> { static constexpr int R = 1, CPB = 4, TP = 0, XSW = 0; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{12, 97, 776}; };
-template <> struct K4C<9> { static constexpr int R = 1, CPB = 3, TP = 0, XSW = 0; static constexpr Lay3 ZY{9, 89, 801}, YX{9, 85, 765}, XZ{9, 81, 729}; };
+template <> struct K4C<3> { static constexpr int R = 1, CPB = 32, CPBS = 20, TP = 0, XSW = 0; static constexpr Lay3 ZY{3, 19, 57}, YX{3, 9, 27}, XZ{3, 18, 57}; };
+template <> struct K4C<4> { static constexpr int R = 2, CPB = 30, CPBS = 18, TP = 0, XSW = 0; static constexpr Lay3 ZY{4, 20, 88}, YX{5, 20, 88}, XZ{5, 20, 84}; };
+template <> struct K4C<5> { static constexpr int R = 2, CPB = 16, CPBS = 11, TP = 0, XSW = 0; static constexpr Lay3 ZY{5, 26, 143}, YX{5, 25, 134}, XZ{5, 25, 139}; };
+template <> struct K4C<6> { static constexpr int R = 1, CPB = 8, CPBS = 5, TP = 0, XSW = 0; static constexpr Lay3 ZY{6, 38, 228}, YX{9, 54, 324}, XZ{11, 66, 402}; };
+template <> struct K4C<7> { static constexpr int R = 2, CPB = 10, CPBS = 4, TP = 0, XSW = 0; static constexpr Lay3 ZY{7, 55, 396}, YX{7, 56, 392}, XZ{7, 49, 344}; };
+template <> struct K4C<8> { static constexpr int R = 1, CPB = 4, CPBS = 3, TP = 0, XSW = 0; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{12, 97, 776}; };
+template <> struct K4C<9> { static constexpr int R = 1, CPB = 3, CPBS = 2, TP = 0, XSW = 0; static constexpr Lay3 ZY{9, 89, 801}, YX{9, 85, 765}, XZ{9, 81, 729}; };
 // alternates (DG_K4_ALT=1): two lines per thread
-template <> struct K4C<6, 1> { static constexpr int R = 2, CPB = 16, TP = 0, XSW = 0; static constexpr Lay3 ZY{6, 38, 242}, YX{9, 54, 338}, XZ{6, 36, 217}; };
-template <> struct K4C<8, 1> { static constexpr int R = 2, CPB = 8, TP = 0, XSW = 0; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{9, 72, 576}; };
+template <> struct K4C<6, 1> { static constexpr int R = 2, CPB = 16, CPBS = 8, TP = 0, XSW = 0; static constexpr Lay3 ZY{6, 38, 242}, YX{9, 54, 338}, XZ{6, 36, 217}; };
+template <> struct K4C<8, 1> { static constexpr int R = 2, CPB = 8, CPBS = 4, TP = 0, XSW = 0; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{9, 72, 576}; };
 // n = 5 alternate: 16 threads per cell (one idle) so that a half-warp never straddles two cells,
 // and the x stage maps thread (a, b) to line (j, k) = (b + r NB, a); with these the Y/X
 // transposes are bank-conflict free (tools/smem_layout_search7.py / smem_ktable_search.py)
-template <> struct K4C<5, 1> { static constexpr int R = 2, CPB = 16, TP = 16, XSW = 1; static constexpr Lay3 ZY{5, 27, 135}, YX{7, 37, 185}, XZ{5, 31, 155}; };
+template <> struct K4C<5, 1> { static constexpr int R = 2, CPB = 16, CPBS = 11, TP = 16, XSW = 1; static constexpr Lay3 ZY{5, 27, 135}, YX{7, 37, 185}, XZ{5, 31, 155}; };
 template <int N> struct K4HasAlt { static constexpr bool value = N == 5 || N == 6 || N == 8; };
 
 constexpr int imax(int a, int b) { return a > b ? a : b; }
@@ -77,7 +82,9 @@ template <int N, int NL, int ALT = 0, int MODE = KMODE_APPLY>
 struct K4Layout {
   // the x->z layout is only used by point Jacobi and by the odd-n Chebyshev order
   static constexpr bool USE_XZ = MODE == KMODE_CHEBY_PJ || (N % 2 == 1 && MODE != KMODE_APPLY);
-  static constexpr int R = K4C<N, ALT>::R, CPB = K4C<N, ALT>::CPB;
+  // K4_STAGE: Chebyshev streams staged in smem (b, u_{j-1}, and dinv unless FDM)
+  static constexpr int NSTG = (K4_STAGE && MODE != KMODE_APPLY) ? (MODE == KMODE_CHEBY_FDM ? 2 : 3) : 0;
+  static constexpr int R = K4C<N, ALT>::R, CPB = NSTG ? K4C<N, ALT>::CPBS : K4C<N, ALT>::CPB;
   static constexpr int NB = (N + R - 1) / R;          // thread rows per cell
   static constexpr int TPC = N * NB;                   // working threads per cell
   static constexpr int TPCP = K4C<N, ALT>::TP ? K4C<N, ALT>::TP : TPC;   // incl. idle padding
@@ -95,7 +102,8 @@ struct K4Layout {
                                      : N * N + 2;
   static constexpr int GYC = 2 * NL * GFS + (N == 3 && NL == 2 ? 1 : 0);
   static constexpr int HS = NL * N * PG;               // one x-halo field [l][k][j]
-  static constexpr int doubles() { return CPB * (S1 + S2 + GYC) + 2 * 2 * HS; }
+  static constexpr int STGOFF = CPB * (S1 + S2 + GYC) + 2 * 2 * HS;   // staging [stream][cell][n^3]
+  static constexpr int doubles() { return STGOFF + (STGOFF & 1) + NSTG * CPB * N * N * N; }
   static constexpr int bytes() { return doubles() * 8; }
 };
 
@@ -159,12 +167,35 @@ __device__ __forceinline__ void pinv_diag(const KP& kp, const T* __restrict__ di
   }
 }
 
+// cp.async (LDGSTS) of W doubles (W = 1: 8 bytes, W = 2: 16 bytes), completion per thread by
+// cp.async.wait_all; used by K4_STAGE to stage the Chebyshev streams at block start
+template <int WB>
+__device__ __forceinline__ void cp_async_w(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  if constexpr (WB == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  else if constexpr (WB == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+}
+
+// read of a staged (shared) or global stream
+template <bool SMEM, typename T>
+__device__ __forceinline__ T ldsrc(const T* p) {
+  if constexpr (SMEM) return *p;
+  else return __ldg(p);
+}
+
 template <typename Real> struct Vec2;
 template <> struct Vec2<double> { using type = double2; };
 template <> struct Vec2<float> { using type = float2; };
 
 template <int N, int NL, int MODE, int OUTD, int ALT, typename Real>
-__global__ void __launch_bounds__(K4Layout<N, NL, ALT>::CPB * K4Layout<N, NL, ALT>::TPCP,
+__global__ void __launch_bounds__(K4Layout<N, NL, ALT, MODE>::CPB * K4Layout<N, NL, ALT, MODE>::TPCP,
                                   (k4_min_blocks<N, NL, ALT, Real, MODE>()))
 k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ GridArgs g,
         const Real* __restrict__ u, Real* __restrict__ y, const __grid_constant__ ChebyArgsT<Real> ch) {
@@ -286,6 +317,27 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       if (!ch.first) l2_prefetch(ch.u_prev + off, cnt, btid, BT);
     }
   }
+  // K4_STAGE: stage the block's tiles of b, u_{j-1} (if read) and dinv in shared memory now;
+  // they are consumed from the X stage on, long after this latency has passed
+  constexpr bool kStage = Lay::NSTG > 0;
+  Real* STG = smem + Lay::STGOFF + (Lay::STGOFF & 1);
+  if constexpr (kStage) {
+    constexpr int W = (N % 2 == 0) ? 2 : 1;                  // doubles per copy (16 / 8 bytes)
+    constexpr int WB = W * (int)sizeof(Real);
+    const int nchunk = ncell * N3 / W;
+    const int64_t off = (rowcell + cx0) * N3;
+    const Real* srcs[3] = {ch.b, ch.u_prev, ch.dinv};
+#pragma unroll
+    for (int st = 0; st < Lay::NSTG; ++st) {
+      if (st == 1 && ch.first) continue;
+      const Real* src = srcs[st] + off;
+      Real* dst = STG + st * CPB * N3;
+      for (int e = btid; e < nchunk; e += BT) cp_async_w<WB>(dst + e * W, src + e * W);
+    }
+  }
+  auto sb = [&]() -> const Real* { return kStage ? STG + cslot * N3 : ch.b + cid * N3; };
+  auto sp = [&]() -> const Real* { return kStage ? STG + (CPB + cslot) * N3 : ch.u_prev + cid * N3; };
+  auto sd = [&]() -> const Real* { return kStage ? STG + (2 * CPB + cslot) * N3 : ch.dinv + cid * N3; };
   // the first job's loads are issued together with the own z-lines
   const Real* jsrc = nullptr;
   Real* jdst = nullptr;
@@ -409,13 +461,14 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
         const int xb = tb + r * NB;
         if (N % R != 0 && xb >= N) break;
         const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
-        const Real* bb = ch.b + cid * N3 + (xk * N + xj) * N;
+        const Real* bb = sb() + (xk * N + xj) * N;
 #pragma unroll
-        for (int i = 0; i < N; ++i) bso[r][i] = __ldg(bb + i);
+        for (int i = 0; i < N; ++i) bso[r][i] = ldsrc<kStage>(bb + i);
       }
     }
   };
   if constexpr (kPreBs && K4_PREB_ODD == 2) load_bso();
+  if constexpr (kStage) cp_async_commit_wait_all();   // own staged chunks landed; the barrier publishes them
   __syncthreads();
   if constexpr (kPreBs && K4_PREB_ODD == 1) load_bso();
 
@@ -431,9 +484,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
         const int xb = tb + r * NB;
         if (N % R != 0 && xb >= N) break;
         const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
-        const Real* bb = ch.b + cid * N3 + (xk * N + xj) * N;
+        const Real* bb = sb() + (xk * N + xj) * N;
 #pragma unroll
-        for (int i = 0; i < N; i += 2) bpre[r][i / 2] = __ldg(reinterpret_cast<const V2*>(bb + i));
+        for (int i = 0; i < N; i += 2) bpre[r][i / 2] = ldsrc<kStage>(reinterpret_cast<const V2*>(bb + i));
       }
     }
   }
@@ -524,7 +577,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
         const int xb = tb + r * NB;
         if (N % R != 0 && xb >= N) break;
         const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
-        const Real* bb = ch.b + cid * N3 + (xk * N + xj) * N;
+        const Real* bb = sb() + (xk * N + xj) * N;
         if constexpr (kPreB) {
 #pragma unroll
           for (int i = 0; i < N; i += 2) {
@@ -537,7 +590,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
           for (int i = 0; i < N; ++i) res[r][i] = bso[r][i] - res[r][i];
         } else {
 #pragma unroll
-          for (int i = 0; i < N; ++i) res[r][i] = __ldg(bb + i) - res[r][i];
+          for (int i = 0; i < N; ++i) res[r][i] = ldsrc<kStage>(bb + i) - res[r][i];
         }
       }
     }
@@ -566,9 +619,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
           for (int r = 0; r < R; ++r) {
             const int zj = tb + r * NB, zi = ta;
             if (N % R != 0 && zj >= N) break;
-            const Real* dv = ch.dinv + cid * N3 + zj * N + zi;
+            const Real* dv = sd() + zj * N + zi;
 #pragma unroll
-            for (int k = 0; k < N; ++k) dpre[r][k] = __ldg(dv + k * NN);
+            for (int k = 0; k < N; ++k) dpre[r][k] = ldsrc<kStage>(dv + k * NN);
           }
         }
       }
@@ -623,7 +676,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
 #pragma unroll
           for (int i = 0; i < N; i += 2) {
             ujpre[r][i / 2] = __ldg(reinterpret_cast<const V2*>(u + gb + i));
-            if (!ch.first) uppre[r][i / 2] = *reinterpret_cast<const V2*>(ch.u_prev + gb + i);
+            if (!ch.first) uppre[r][i / 2] = *reinterpret_cast<const V2*>(sp() + (gb - cid * N3) + i);
           }
         }
       }
@@ -696,9 +749,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
           for (int r = 0; r < R; ++r) {
             const int yk = tb + r * NB, yi = ta;
             if (N % R != 0 && yk >= N) break;
-            const Real* dv = ch.dinv + cid * N3 + yk * NN + yi;
+            const Real* dv = sd() + yk * NN + yi;
 #pragma unroll
-            for (int j = 0; j < N; ++j) dpre[r][j] = __ldg(dv + j * N);
+            for (int j = 0; j < N; ++j) dpre[r][j] = ldsrc<kStage>(dv + j * N);
           }
         }
       }
@@ -748,7 +801,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
 #pragma unroll
           for (int k = 0; k < N; ++k) {
             ujz[r][k] = __ldg(u + gbase + k * NN);
-            if (!ch.first) upz[r][k] = ch.u_prev[gbase + k * NN];
+            if (!ch.first) upz[r][k] = sp()[gbase - cid * N3 + k * NN];
           }
         }
       }
@@ -796,9 +849,9 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
           const int xb = tb + r * NB;
           if (N % R != 0 && xb >= N) break;
           const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
-          const Real* dv = ch.dinv + cid * N3 + (xk * N + xj) * N;
+          const Real* dv = sd() + (xk * N + xj) * N;
 #pragma unroll
-          for (int i = 0; i < N; ++i) X1[at(LXZ, i, xj, xk)] = res[r][i] * __ldg(dv + i);
+          for (int i = 0; i < N; ++i) X1[at(LXZ, i, xj, xk)] = res[r][i] * ldsrc<kStage>(dv + i);
         }
       }
       __syncthreads();
@@ -824,7 +877,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
           const int64_t gi = gbase + k * NN;
           const Real uj = __ldg(u + gi);   // re-read (L1/L2): saves R*N live registers
           Real v = fma((Real)ch.c_z, res[r][k], uj);
-          if (!ch.first) v = fma((Real)ch.c_prev, uj - ch.u_prev[gi], v);
+          if (!ch.first) v = fma((Real)ch.c_prev, uj - sp()[gi - cid * N3], v);
           ch.u_next[gi] = v;
         }
       }

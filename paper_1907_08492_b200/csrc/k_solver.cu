@@ -150,6 +150,11 @@ __global__ void k_d2f(const double* __restrict__ in, float* __restrict__ out, in
     out[i] = (float)in[i];
 }
 
+__global__ void k_f2d(const float* __restrict__ in, double* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (double)in[i];
+}
+
 template <int N, int INNER>
 cudaError_t launch_pinv_n(const KronParams& kp, const double* r, const double* dinv, double* z, int64_t ncells,
                           cudaStream_t s) {
@@ -194,6 +199,12 @@ int dot_partials() { return kDotBlocks; }
 cudaError_t launch_d2f(const double* in, float* out, int64_t n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   k_d2f<<<148 * 8, 256, 0, s>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_f2d(const float* in, double* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_f2d<<<148 * 8, 256, 0, s>>>(in, out, n);
   return cudaGetLastError();
 }
 
