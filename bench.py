@@ -81,10 +81,13 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()   # nvidia-smi takes a moment to start: wait for its first sample
+            while not self.lines and time.time() - t0 < 3.0:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
@@ -391,8 +394,12 @@ def run_ours(a, rank, world, local_rank):
         return float(t.item())
 
     fp64_peak = None
+    fp64_peaks = {}
     if not a.quick:
         fp64_peak = P.measure_peak("fp64")
+        # the FP64 tensor cores (DMMA) against the DFMA roof, measured
+        fp64_peaks = {"dfma_tflops": fp64_peak, "dmma_tflops": P.measure_peak("dmma"),
+                      "dmma_and_dfma_interleaved_tflops": P.measure_peak("dmma+dfma")}
     # ---------------------------------------------------------------- setup per degree
     nccl_id = None
     if world > 1:   # one unique id: every degree's mesh shares one NCCL communicator
@@ -462,6 +469,7 @@ def run_ours(a, rank, world, local_rank):
     matvec_roof = {"achieved_gbs": mv_gbs, "frac_hbm": mv_gbs / hbm_peak}
     if fp64_peak:
         matvec_roof["fp64_peak_tflops_measured"] = fp64_peak
+        matvec_roof["fp64_peaks_measured"] = fp64_peaks
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",

@@ -282,7 +282,11 @@ dg_status dg_tables_1d(int32_t degree, int32_t basis, double penalty_factor, dou
 /* Machine characterisation (roofline denominators measured on the running GPU):
  * kind 0: fp64 FMA throughput in TFLOP/s (DFMA chains, 148*8 blocks);
  * kind 1: streaming copy bandwidth in GB/s (read + write bytes, 2 GiB buffers);
- * kind 2: streaming read bandwidth in GB/s.  Best of 5 timed launches. */
+ * kind 2: streaming read bandwidth in GB/s;
+ * kind 3: fp64 tensor-core throughput in TFLOP/s (DMMA, mma.sync m8n8k4 f64 chains);
+ * kind 4: DMMA chains and DFMA chains interleaved in one kernel, total TFLOP/s (if the two
+ *         used separate pipes this would approach the sum of kinds 0 and 3).
+ * Best of 5 timed launches. */
 dg_status dg_measure_peak(int32_t kind, double* value, void* stream);
 
 /* Number of kernels this library launched since the handle was created. */

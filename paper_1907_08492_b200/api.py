@@ -64,9 +64,10 @@ def get_nccl_unique_id() -> bytes:
 
 
 def measure_peak(kind: str, stream=None) -> float:
-    """'fp64' -> TFLOP/s of DFMA; 'copy' / 'read' -> GB/s (see dg_measure_peak)."""
+    """'fp64' -> TFLOP/s of DFMA; 'copy' / 'read' -> GB/s; 'dmma' -> fp64 tensor-core TFLOP/s;
+    'dmma+dfma' -> both interleaved (see dg_measure_peak)."""
     v = ctypes.c_double()
-    _check(lib().dg_measure_peak({"fp64": 0, "copy": 1, "read": 2}[kind], ctypes.byref(v),
+    _check(lib().dg_measure_peak({"fp64": 0, "copy": 1, "read": 2, "dmma": 3, "dmma+dfma": 4}[kind], ctypes.byref(v),
                                  _stream(stream)), "dg_measure_peak")
     return v.value
 

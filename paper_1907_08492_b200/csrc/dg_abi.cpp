@@ -258,13 +258,20 @@ dg_status post_launch(dg_mesh m, cudaError_t e, const char* what, cudaStream_t s
   return DG_OK;
 }
 
-// Cartesian kernel selection: k_kron4 (z-first) unless DG_KRON=3 asks for k_kron.cu
-bool kron_v4(int n) {
-  static const int v = [] {
-    const char* e = std::getenv("DG_KRON");
-    return e ? std::atoi(e) : 4;
+// Cartesian kernel selection: k_kron4 (z-first) for p = 2..8; p = 1 runs the general
+// quadrature kernel k_quad on the constant geometry (the same operator)
+bool kron_v4(int n) { return kron4_supported(n); }
+
+// Cartesian matvec kernel: k_kron6 (i-plane schedule) where DG_K6 selects it for this n
+// (bit n-3 of the mask; see DESIGN.md for the measured choice), else k_kron4
+bool kron6_use(int n, int NL, int mode) {
+  static const int mask = [] {
+    const char* e = std::getenv("DG_K6");
+    return e ? std::atoi(e) : 1;   // measured: k_kron6 wins only for the n = 3 matvec
   }();
-  return v != 3 && kron4_supported(n);
+  // bits 0-3: matvec at n = 3..6; bits 4-7: the fused Chebyshev step at n = 3..6
+  const int bit = (mode == KMODE_APPLY ? 0 : 4) + (n - 3);
+  return kron6_supported(n, NL, mode) && ((mask >> bit) & 1);
 }
 
 // general kernel selection: k_quad3 (z-first) unless DG_QUAD=1 asks for k_quad.cu
@@ -885,7 +892,7 @@ dg_status dg_halo_set(dg_mesh m, const double* recv_lo, const double* recv_hi, v
 }
 
 dg_status dg_measure_peak(int32_t kind, double* value, void* stream) {
-  if (!value || kind < 0 || kind > 2) return fail(DG_ERR_PARAM, "bad kind or NULL value");
+  if (!value || kind < 0 || kind > 4) return fail(DG_ERR_PARAM, "bad kind or NULL value");
   CUDA_TRY(measure_peak(kind, value, (cudaStream_t)stream));
   return DG_OK;
 }
@@ -1121,10 +1128,10 @@ dg_status run_pass(dg_mesh m, int mode, bool kron, const double* u, double* y, c
     if (ze <= zb) return DG_OK;
     GridArgs g = grid_args(m, zb, ze);
     cudaError_t e;
-    if (kron && kron_v4(m->n))
+    if (kron && kron6_use(m->n, m->NL, mode))
+      e = launch_kron6(m->n, mode, m->kp, g, u, y, ch, s);
+    else if (kron && kron_v4(m->n))
       e = launch_kron4(m->n, m->NL, mode, m->kp, g, u, y, ch, s);
-    else if (kron)
-      e = launch_kron(m->n, m->NL, mode, m->kp, g, u, y, ch, s);
     else if (quad_v3(m->n, m->geom))
       e = launch_quad3(m->n, m->NL, m->geom, mode, m->qp, m->ga, g, u, y, ch, s);
     else
@@ -1559,10 +1566,10 @@ dg_status launch_apply_range(dg_mesh m, bool kron, const double* u, double* y, i
   GridArgs g = grid_args(m, zb, ze);
   ChebyArgs ch{};
   cudaError_t e;
-  if (kron && kron_v4(m->n))
+  if (kron && kron6_use(m->n, m->NL, KMODE_APPLY))
+    e = launch_kron6(m->n, KMODE_APPLY, m->kp, g, u, y, ch, s);
+  else if (kron && kron_v4(m->n))
     e = launch_kron4(m->n, m->NL, KMODE_APPLY, m->kp, g, u, y, ch, s);
-  else if (kron)
-    e = launch_kron(m->n, m->NL, KMODE_APPLY, m->kp, g, u, y, ch, s);
   else if (quad_v3(m->n, m->geom))
     e = launch_quad3(m->n, m->NL, m->geom, KMODE_APPLY, m->qp, m->ga, g, u, y, ch, s);
   else

@@ -115,13 +115,15 @@ struct MapParams {
   double xq[kMaxN], wq[kMaxN];
 };
 
-// Launchers (k_kron.cu, k_basis_change.cu, k_setup.cu)
-cudaError_t launch_kron(int n, int NL, int mode, const KronParams& kp, const GridArgs& g,
-                        const double* u, double* y, const ChebyArgs& ch, cudaStream_t s);
+// Launchers (k_kron4.cu, k_kron6.cu, k_basis_change.cu, k_setup.cu)
 // z-first Kronecker kernel (k_kron4.cu), the default Cartesian path for n = 3..9
 bool kron4_supported(int n);
 cudaError_t launch_kron4(int n, int NL, int mode, const KronParams& kp, const GridArgs& g,
                          const double* u, double* y, const ChebyArgs& ch, cudaStream_t s);
+// i-plane Cartesian matvec (k_kron6.cu): z and y sweeps of a whole (j,k) plane per thread
+bool kron6_supported(int n, int NL, int mode);
+cudaError_t launch_kron6(int n, int mode, const KronParams& kp, const GridArgs& g, const double* u, double* y,
+                         const ChebyArgs& ch, cudaStream_t s);
 cudaError_t launch_kron4_f32(int n, int NL, int mode, const KronParamsF& kp, const GridArgs& g,
                              const float* u, float* y, const ChebyArgsF& ch, cudaStream_t s);
 // z-first basis change (k_kron4.cu), n = 3..9; in == out is NOT allowed (z-lines are read

@@ -1,6 +1,6 @@
 // Cartesian fast path of the SIPG operator, z-first schedule (k_kron4).
 //
-// Same operator as k_kron.cu: on a Cartesian cell the quadrature operator of Eq. (1)
+// On a Cartesian cell the quadrature operator of Eq. (1)
 // equals the Kronecker form of Eq. (14) (the paper names the
 // reference-coordinate form at PAPER.md:336-344):
 //   y_K = (M (x) M (x) L_z + M (x) L_y (x) M + L_x (x) M (x) M) u_K
@@ -1049,378 +1049,14 @@ cudaError_t launch_bchg4_n(const BchgParams& bp, const double* in, double* out, 
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------- k_kron5
-// Persistent z-marching form of the k_kron4 matvec (opt-in, DG_K5=1; even n, NL = 2, fp64):
-// a block owns an x-run of one row for ZC consecutive planes.  The own tile of the next plane
-// is fetched by a bulk asynchronous copy (cp.async.bulk, completed on an mbarrier) into a
-// shared-memory buffer while the current plane's Y and X stages run, and the z- ghost layers
-// are carried in registers from the previous plane (no z- re-read).  Stages as in k_kron4.
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n K5WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra K5WAIT%=;\n}\n" ::"r"(
-          smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-#ifndef K5_MIN_BLOCKS
-#define K5_MIN_BLOCKS 2   // measured: 3 blocks/SM spills 128-416 B and runs 1.2-1.6x slower
-#endif
-template <int N>
-__global__ void __launch_bounds__(K4Layout<N, 2>::CPB * K4Layout<N, 2>::TPC, K5_MIN_BLOCKS)
-k_kron5(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g, const double* __restrict__ u,
-        double* __restrict__ y, int zc) {
-  using Real = double;
-  constexpr int NL = 2;
-  using Lay = K4Layout<N, NL, 0, KMODE_APPLY>;
-  constexpr int R = Lay::R, NB = Lay::NB, TPC = Lay::TPC, CPB = Lay::CPB;
-  constexpr int NN = N * N, N3 = N * NN;
-  constexpr Lay3 LZY = Lay::ZY, LYX = Lay::YX;
-  constexpr int PG = Lay::PG, GPG = Lay::GPG, GFS = Lay::GFS;
-  static_assert(N % 2 == 0, "k_kron5: even n (16-byte aligned cell tiles)");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Real* R1 = reinterpret_cast<Real*>(smem_raw);
-  Real* R2 = R1 + CPB * Lay::S1;
-  Real* GYb = R2 + CPB * Lay::S2;
-  Real* HX = GYb + CPB * Lay::GYC;
-  Real* UB = HX + 2 * 2 * Lay::HS;                                       // own tile [cell][n^3]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(UB + CPB * N3 + (CPB * N3) % 2);
-
-  const int ta = threadIdx.x, cslot = threadIdx.y / NB, tb = threadIdx.y - cslot * NB;
-  const int cx0 = blockIdx.x * CPB;
-  const int cy = blockIdx.y;
-  const int ncell = g.Nx - cx0 < CPB ? g.Nx - cx0 : CPB;
-  const bool active = cslot < ncell;
-  const int cx = cx0 + cslot;
-  const int64_t plane = (int64_t)g.Nx * g.Ny;
-  const int z0 = g.zbeg + blockIdx.z * zc;
-  const int z1 = z0 + zc < g.zend ? z0 + zc : g.zend;
-  constexpr int BT = CPB * TPC;
-  const int btid = threadIdx.x + N * threadIdx.y;
-  const unsigned tile_bytes = (unsigned)(ncell * N3 * sizeof(Real));
-  Real* GY = GYb + cslot * Lay::GYC;
-
-  const bool xper = g.bc[0] == DG_BC_PERIODIC;
-  int h0 = cx0 > 0 ? cx0 - 1 : (xper ? g.Nx - 1 : -1);
-  int h1 = cx0 + ncell < g.Nx ? cx0 + ncell : (xper ? 0 : -1);
-  if (ncell == g.Nx) h0 = h1 = -1;
-  const bool need_h0 = cslot == 0 && h0 >= 0;
-  const bool need_h1 = cslot == ncell - 1 && h1 >= 0;
-  const bool yper = g.bc[1] == DG_BC_PERIODIC;
-  const int ym_row = cy > 0 ? cy - 1 : (yper ? g.Ny - 1 : -1);
-  const int yp_row = cy + 1 < g.Ny ? cy + 1 : (yper ? 0 : -1);
-  constexpr int NYJ = 2 * NL * N;
-  const int nyj = ncell * NYJ;
-  const int nh0 = h0 >= 0 ? NL * N : 0, nh1 = h1 >= 0 ? NL * N : 0;
-  const int njobs = nyj + nh0 + nh1;
-
-  if (btid == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (btid == 0 && z0 < z1) {
-    mbar_arrive_expect_tx(bar, tile_bytes);
-    bulk_g2s(UB, u + (((int64_t)z0 * g.Ny + cy) * g.Nx + cx0) * N3, tile_bytes, bar);
-  }
-  Real zcarry[R][NL];   // layers n-NL.. of the previous plane's own z-lines
-  unsigned phase = 0;
-#pragma unroll 1
-  for (int cz = z0; cz < z1; ++cz) {
-    // coefficient pointers re-derived every plane through an opaque zero, so that the
-    // compiler keeps loading the 1D matrices from the constant bank where they are used
-    // instead of hoisting all of them into registers for the whole z loop
-    const int oz = cz < 0 ? cz : 0;   // 0 (cz >= 0), but not provably so for the compiler
-    const double* cM = kp.M + oz;
-    const double* cL0 = kp.L[0] + oz;
-    const double* cL1 = kp.L[1] + oz;
-    const double* cL2 = kp.L[2] + oz;
-    const double* cNm0 = kp.Nm[0] + oz;
-    const double* cNm1 = kp.Nm[1] + oz;
-    const double* cNm2 = kp.Nm[2] + oz;
-    const double* cNp0 = kp.Np[0] + oz;
-    const double* cNp1 = kp.Np[1] + oz;
-    const double* cNp2 = kp.Np[2] + oz;
-    const int64_t rowcell = ((int64_t)cz * g.Ny + cy) * g.Nx;
-    const int64_t cid = rowcell + cx;
-    const Real* ucell = u + cid * N3;
-    // z ghost sources: z- carried unless this is the block's first plane
-    int zsrc[2];
-    const Real* zbase[2];
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int nz = cz + (s ? 1 : -1);
-      if (nz >= 0 && nz < g.nz) {
-        zsrc[s] = ZSRC_LOCAL;
-        zbase[s] = ucell + (s ? plane * N3 : -plane * N3);
-      } else {
-        zsrc[s] = s ? g.zhi : g.zlo;
-        zbase[s] = ucell + (s ? -(int64_t)(g.nz - 1) : (int64_t)(g.nz - 1)) * plane * N3;
-        if (zsrc[s] == ZSRC_HALO)
-          zbase[s] = (s ? g.halo_hi : g.halo_lo) + ((int64_t)cy * g.Nx + cx) * (NL * NN) - (s ? 0 : (N - NL) * NN);
-      }
-    }
-    const bool carried = cz > z0;
-    // plane cz+2 into L2 now: its layers 0..NL-1 are the z+ ghosts of the next plane, and the
-    // y-neighbour blocks read their ghost z-lines of plane cz+1 from the tiles prefetched here
-    // (only planes of this block's chunk: a plane beyond it is read much later by another block)
-    if (g.l2pf && cz + 2 < z1) l2_prefetch(u + (rowcell + 2 * plane + cx0) * N3, (int64_t)ncell * N3, btid, BT);
-    else if (g.l2pf && cz == z0 && cz + 1 < z1) l2_prefetch(u + (rowcell + plane + cx0) * N3, (int64_t)ncell * N3, btid, BT);
-    auto job_target = [&](int job, const Real*& src, Real*& dst, int& ds) {
-      if (job < nyj) {
-        const int c = job / NYJ, jj = job - c * NYJ;
-        const int f = jj / (NL * N), l = (jj / N) % NL, i = jj % N;
-        const int nrow = f ? yp_row : ym_row;
-        if (nrow < 0) {
-          src = nullptr;
-          return;
-        }
-        const int jl = f ? l : N - NL + l;
-        src = u + (((int64_t)cz * g.Ny + nrow) * g.Nx + cx0 + c) * N3 + jl * N + i;
-        dst = GYb + c * Lay::GYC + (f * NL + l) * GFS + i;
-        ds = GPG;
-      } else {
-        const int hj = job - nyj;
-        const int h = hj < nh0 ? 0 : 1;
-        const int q = hj - (h ? nh0 : 0);
-        const int l = q / N, j = q - l * N;
-        const int il = h == 0 ? N - NL + l : l;
-        src = u + (rowcell + (h ? h1 : h0)) * N3 + j * N + il;
-        dst = HX + ((h * 2 + 0) * NL + l) * N * PG + j;
-        ds = PG;
-      }
-    };
-    // ============================================================ Z
-    const Real* jsrc = nullptr;
-    Real* jdst = nullptr;
-    int jds = PG;
-    Real jv[N];
-    if (btid < njobs) job_target(btid, jsrc, jdst, jds);
-    if (jsrc) {
-#pragma unroll
-      for (int k = 0; k < N; ++k) jv[k] = __ldg(jsrc + k * NN);
-    }
-    Real zpv[R][NL], zmv[R][NL];
-    if (active) {   // ghost loads before waiting for the tile
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int zj = tb + r * NB, zi = ta;
-        if (N % R != 0 && zj >= N) break;
-#pragma unroll
-        for (int l = 0; l < NL; ++l) {
-          const int Lm = N - NL + l, Lp = l;
-          zpv[r][l] = zsrc[1] == ZSRC_MIRROR ? 0.0 : __ldg(zbase[1] + Lp * NN + zj * N + zi);
-          zmv[r][l] = carried ? zcarry[r][l]
-                              : (zsrc[0] == ZSRC_MIRROR ? 0.0 : __ldg(zbase[0] + Lm * NN + zj * N + zi));
-        }
-      }
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    if (active) {
-      const Real* ut = UB + cslot * N3;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int zj = tb + r * NB;
-        if (N % R != 0 && zj >= N) break;
-        const int zi = ta;
-        Real uz[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) uz[k] = ut[k * NN + zj * N + zi];
-        Real zm[NL], zp[NL];
-#pragma unroll
-        for (int l = 0; l < NL; ++l) {
-          const int Lm = N - NL + l, Lp = l;
-          zm[l] = (!carried && zsrc[0] == ZSRC_MIRROR) ? -uz[N - 1 - Lm] : zmv[r][l];
-          zp[l] = zsrc[1] == ZSRC_MIRROR ? -uz[N - 1 - Lp] : zpv[r][l];
-          zcarry[r][l] = uz[N - NL + l];
-        }
-        Real t[N], a[N];
-        const auto su = eo_split<N>(uz);
-        eo_mul<N, 1, false>(cM, su, t);
-        eo_mul<N, 1, false>(cL2, su, a);
-        dense_add<NL, NL>(cNm2, zm, &a[0]);
-        dense_add<NL, NL>(cNp2, zp, &a[N - NL]);
-        Real* T = R1 + cslot * LZY.CS;
-        Real* A = R2 + cslot * LZY.CS;
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          T[at(LZY, zi, zj, k)] = t[k];
-          A[at(LZY, zi, zj, k)] = a[k];
-        }
-      }
-    }
-    if (jsrc) {
-      Real o[N];
-      eo_apply<N, 1>(cM, jv, o);
-#pragma unroll
-      for (int k = 0; k < N; ++k) jdst[k * jds] = o[k];
-    }
-#pragma unroll 1
-    for (int job = btid + BT; job < njobs; job += BT) {
-      const Real* src;
-      Real* dst;
-      int ds = PG;
-      job_target(job, src, dst, ds);
-      if (src) mass_line<N>(cM, src, NN, dst, ds);
-    }
-    __syncthreads();   // the own tile is consumed: fetch the next plane's
-    if (btid == 0 && cz + 1 < z1) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(bar, tile_bytes);
-      bulk_g2s(UB, u + (rowcell + plane + cx0) * N3, tile_bytes, bar);
-    }
-    // ============================================================ Y
-    {
-      Real bl[R][N], cl[R][N];
-      if (active) {
-        const Real* T = R1 + cslot * LZY.CS;
-        const Real* A = R2 + cslot * LZY.CS;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int yk = tb + r * NB, yi = ta;
-          if (N % R != 0 && yk >= N) break;
-          Real al[N], tl[N];
-#pragma unroll
-          for (int j = 0; j < N; ++j) {
-            al[j] = A[at(LZY, yi, j, yk)];
-            tl[j] = T[at(LZY, yi, j, yk)];
-          }
-          Real gym[NL], gyp[NL];
-#pragma unroll
-          for (int l = 0; l < NL; ++l) {
-            gym[l] = ym_row >= 0 ? GY[(0 * NL + l) * GFS + yk * GPG + yi] : -tl[NL - 1 - l];
-            gyp[l] = yp_row >= 0 ? GY[(1 * NL + l) * GFS + yk * GPG + yi] : -tl[N - 1 - l];
-          }
-          const auto st = eo_split<N>(tl);
-          eo_mul2<N, 1>(cM, eo_split<N>(al), cL1, st, bl[r]);
-          eo_mul<N, 1, false>(cM, st, cl[r]);
-          dense_add<NL, NL>(cNm1, gym, &bl[r][0]);
-          dense_add<NL, NL>(cNp1, gyp, &bl[r][N - NL]);
-        }
-      }
-      for (int job = btid; job < nh0 + nh1; job += BT) {
-        const int h = job < nh0 ? 0 : 1;
-        const int q = job - (h ? nh0 : 0);
-        const int l = q / N, k = q - l * N;
-        mass_line<N>(cM, HX + (((h * 2 + 0) * NL + l) * N + k) * PG, 1,
-                     HX + (((h * 2 + 1) * NL + l) * N + k) * PG, 1);
-      }
-      __syncthreads();
-      if (active) {
-        Real* Bf = R1 + cslot * LYX.CS;
-        Real* Cf = R2 + cslot * LYX.CS;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int yk = tb + r * NB, yi = ta;
-          if (N % R != 0 && yk >= N) break;
-#pragma unroll
-          for (int j = 0; j < N; ++j) {
-            Bf[at(LYX, yi, j, yk)] = bl[r][j];
-            Cf[at(LYX, yi, j, yk)] = cl[r][j];
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // ============================================================ X (direct 128-bit stores)
-    if (active) {
-      const Real* Bf = R1 + cslot * LYX.CS;
-      const Real* Cf = R2 + cslot * LYX.CS;
-      const bool inb_m = cslot > 0, inb_p = cslot + 1 < ncell;
-      const bool wrap = xper && ncell == g.Nx;
-      const int offm = inb_m ? -LYX.CS : (ncell - 1) * LYX.CS;
-      const int offp = inb_p ? LYX.CS : -(ncell - 1) * LYX.CS;
-      const bool slot_m = inb_m || wrap, slot_p = inb_p || wrap;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int xk = tb + r * NB, xj = ta;
-        if (N % R != 0 && xk >= N) break;
-        Real bl[N], cl[N], res[N];
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-          bl[i] = Bf[at(LYX, i, xj, xk)];
-          cl[i] = Cf[at(LYX, i, xj, xk)];
-        }
-        Real cxm[NL], cxp[NL];
-#pragma unroll
-        for (int l = 0; l < NL; ++l) {
-          const int Lm = N - NL + l, Lp = l;
-          cxm[l] = slot_m ? Cf[offm + at(LYX, Lm, xj, xk)]
-                          : (need_h0 ? HX[(((0 * 2 + 1) * NL + l) * N + xk) * PG + xj] : -cl[N - 1 - Lm]);
-          cxp[l] = slot_p ? Cf[offp + at(LYX, Lp, xj, xk)]
-                          : (need_h1 ? HX[(((1 * 2 + 1) * NL + l) * N + xk) * PG + xj] : -cl[N - 1 - Lp]);
-        }
-        eo_mul2<N, 1>(cM, eo_split<N>(bl), cL0, eo_split<N>(cl), res);
-        dense_add<NL, NL>(cNm0, cxm, &res[0]);
-        dense_add<NL, NL>(cNp0, cxp, &res[N - NL]);
-        Real* out = y + cid * N3 + (xk * N + xj) * N;
-#pragma unroll
-        for (int i = 0; i < N; i += 2) *reinterpret_cast<double2*>(out + i) = make_double2(res[i], res[i + 1]);
-      }
-    }
-    __syncthreads();   // B, C, GY, HX of this plane consumed before the next plane's Z stage
-  }
-}
-
-template <int N>
-cudaError_t launch_kron5_n(const KronParams& kp, const GridArgs& g, const double* u, double* y, cudaStream_t s) {
-  using Lay = K4Layout<N, 2, 0, KMODE_APPLY>;
-  const int planes = g.zend - g.zbeg;
-  if (planes <= 0 || g.Nx <= 0 || g.Ny <= 0) return cudaSuccess;
-  static const int zc = [] {
-    const char* e = std::getenv("DG_K5_ZC");
-    return e ? std::max(1, std::atoi(e)) : 8;
-  }();
-  const int nzc = (planes + zc - 1) / zc;
-  if (g.Ny > 65535 || nzc > 65535) return cudaErrorInvalidValue;
-  const dim3 grid((g.Nx + Lay::CPB - 1) / Lay::CPB, g.Ny, nzc);
-  const dim3 block(N, Lay::NB * Lay::CPB);
-  const size_t smem = (size_t)(Lay::doubles() + Lay::CPB * N * N * N + 2) * sizeof(double) + 16;
-  auto kern = k_kron5<N>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kern<<<grid, block, smem, s>>>(kp, g, u, y, zc);
-  return cudaGetLastError();
-}
-
 }  // namespace
 
-// n in 3..9 (p = 2..8); other degrees use k_kron.cu
+// n in 3..9 (p = 2..8); p = 1 uses the general quadrature kernel k_quad
 bool kron4_supported(int n) { return n >= 3 && n <= 9; }
 
 template <typename Real>
 cudaError_t launch_kron4_t(int n, int NL, int mode, const KronParamsT<Real>& kp, const GridArgs& g, const Real* u,
                            Real* y, const ChebyArgsT<Real>& ch, cudaStream_t s) {
-  if constexpr (std::is_same<Real, double>::value) {   // opt-in z-marching matvec (DG_K5=1)
-    static const bool k5 = [] {
-      const char* e = std::getenv("DG_K5");
-      return e && std::atoi(e) == 1;
-    }();
-    if (k5 && mode == KMODE_APPLY && NL == 2) {
-      switch (n) {
-        case 4: return launch_kron5_n<4>(kp, g, u, y, s);
-        case 6: return launch_kron5_n<6>(kp, g, u, y, s);
-        case 8: return launch_kron5_n<8>(kp, g, u, y, s);
-      }
-    }
-  }
   switch (n) {
     case 3: return launch_nl<3, Real>(NL, mode, kp, g, u, y, ch, s);
     case 4: return launch_nl<4, Real>(NL, mode, kp, g, u, y, ch, s);

@@ -18,7 +18,7 @@
 //   Z   g = (S c1, S c2, DS c3); t = G_q g; d = (S^T t_x, S^T t_y, DS^T t_z)
 //   YT  e1 = S^T d1, e2 = DS^T d2 + S^T d3
 //   XT  y = DS^T e1 + S^T e2 + face injections of R0, R1 (single write)
-// The fused Chebyshev variants continue from XT in registers (as k_kron.cu).
+// The fused Chebyshev variants continue from XT in registers.
 #include <cuda_runtime.h>
 
 #include "common.cuh"

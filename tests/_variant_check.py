@@ -28,7 +28,7 @@ def dev(x):
 
 def main(degrees, curved):
     for p in degrees:
-        for nc, bcx in (((19, 3, 2), "periodic"), ((21, 2, 3), "dirichlet")):
+        for nc, bcx in (((19, 3, 2), "periodic"), ((21, 2, 3), "dirichlet"), ((45, 2, 2), "periodic")):
             geoms = [("constant", 0.0)] + ([("per_qpoint", 0.03)] if curved else [])
             for geom, amp in geoms:
                 spec = MeshSpec(degree=p, n_cells=nc, bc=(bcx, "periodic", "dirichlet"), geometry=geom,
@@ -39,6 +39,8 @@ def main(degrees, curved):
                 u = uniform_vector(spec.n_dofs, spec.seed)
                 e = rel(m.apply_laplace(dev(u)).cpu().numpy(), H.apply(u))
                 assert e <= TOL, (p, nc, geom, "apply", e)
+                if nc[0] == 45:   # rows of several blocks with a periodic wrap between blocks
+                    continue
                 b = uniform_vector(spec.n_dofs, 710 + p)
                 cheb = p <= 5 and nc[0] == 19   # the oracle smoother setup is slow beyond that
                 for inner, Pc in ((("gl_jacobi", sm.GLJacobi(SIPG(om, p, "gl"))),

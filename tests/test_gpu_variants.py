@@ -1,8 +1,8 @@
 """The opt-in kernel variants (selected by environment variables the library reads once per
 process) against the oracle, each in its own subprocess (tests/_variant_check.py): the
-previous x-first Cartesian kernel, the k_quad general kernel, the n = 5/6/8 alternates of
-k_kron4, the other output path of k_kron4, the z-first basis change at every degree, the
-L2-prefetch settings and the experimental z-marching matvec k_kron5.  The defaults are covered by test_gpu_parity.py."""
+k_quad general kernel, the n = 5/6/8 alternates of k_kron4, the other output path of
+k_kron4, the z-first basis change at every degree, the L2-prefetch settings and the
+i-plane kernel k_kron6 on and off.  The defaults are covered by test_gpu_parity.py."""
 import os
 import subprocess
 import sys
@@ -15,7 +15,6 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 VARIANTS = [
-    ({"DG_KRON": "3"}, "2,5", False),
     ({"DG_QUAD": "1"}, "3", True),
     ({"DG_K4_ALT": "1"}, "4,5,7", False),
     ({"DG_K4_OUT": "0"}, "3,5", False),
@@ -25,8 +24,8 @@ VARIANTS = [
     ({"DG_L2PF": "0"}, "5", False),
     ({"DG_L2PF": "2"}, "4", False),
     ({"DG_L2PF": "3"}, "3,6", False),
-    ({"DG_K5": "1"}, "3,5,7", False),
-    ({"DG_K5": "1", "DG_K5_ZC": "2"}, "3,7", False),
+    ({"DG_K6": "255"}, "2,3,4,5", False),     # k_kron6 i-plane matvec + Chebyshev for n = 3..6
+    ({"DG_K6": "0"}, "2,3,4,5", False),       # k_kron4 for every n
 ]
 
 
