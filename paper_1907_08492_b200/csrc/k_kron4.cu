@@ -74,7 +74,11 @@ template <> struct K4C<8, 1> { static constexpr int R = 2, CPB = 8, CPBS = 4, TP
 // and the x stage maps thread (a, b) to line (j, k) = (b + r NB, a); with these the Y/X
 // transposes are bank-conflict free (tools/smem_layout_search7.py / smem_ktable_search.py)
 template <> struct K4C<5, 1> { static constexpr int R = 2, CPB = 16, CPBS = 11, TP = 16, XSW = 1; static constexpr Lay3 ZY{5, 27, 135}, YX{7, 37, 185}, XZ{5, 31, 155}; };
-template <int N> struct K4HasAlt { static constexpr bool value = N == 5 || N == 6 || N == 8; };
+// n = 3 alternate: 12 threads per cell (3 idle: they take block jobs) so that all three
+// transposes are bank-conflict free (the unpadded y->x layout costs 2x; ncu: 25 % of the
+// Chebyshev step's shared wavefronts were conflicts, LSU pipe 87 %)
+template <> struct K4C<3, 1> { static constexpr int R = 1, CPB = 24, CPBS = 16, TP = 12, XSW = 0; static constexpr Lay3 ZY{3, 19, 57}, YX{4, 19, 57}, XZ{3, 9, 27}; };
+template <int N> struct K4HasAlt { static constexpr bool value = N == 3 || N == 5 || N == 6 || N == 8; };
 
 constexpr int imax(int a, int b) { return a > b ? a : b; }
 
@@ -909,12 +913,12 @@ cudaError_t launch_mode(int mode, const KronParamsT<Real>& kp, const GridArgs& g
     const char* e = std::getenv("DG_K4_OUT");
     return e ? std::atoi(e) : (N % 2 == 0 ? 1 : 0);   // measured: direct wins for even n only
   }();
-  static const int alt = [] {   // DG_K4_ALT=1: the alternate configuration (n = 5, 6, 8)
+  static const int alt_mask = [] {   // DG_K4_ALT: bit n-3 selects the alternate configuration
     const char* e = std::getenv("DG_K4_ALT");
     return e ? std::atoi(e) : 0;
   }();
   if constexpr (K4HasAlt<N>::value) {
-    if (alt == 1) {
+    if ((alt_mask >> (N - 3)) & 1) {
       switch (mode) {
         case KMODE_APPLY:
           return outd ? launch_t<N, NL, KMODE_APPLY, 1, 1, Real>(kp, g, u, y, ch, s)

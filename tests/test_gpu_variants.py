@@ -16,7 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 VARIANTS = [
     ({"DG_QUAD": "1"}, "3", True),
-    ({"DG_K4_ALT": "1"}, "4,5,7", False),
+    ({"DG_K4_ALT": "44"}, "4,5,7", False),   # alternates at n = 5, 6, 8 (bits n-3)
+    ({"DG_K4_ALT": "1"}, "2", False),        # n = 3 alternate (padded threads)
     ({"DG_K4_OUT": "0"}, "3,5", False),
     ({"DG_K4_OUT": "1"}, "2,4", False),
     ({"DG_BCHG": "4"}, "1,3,4,5,6,7", False),
