@@ -6,8 +6,9 @@
 // y = A x needs 2 (n/2)^2 FMAs plus about 2n additions instead of n^2 FMAs.
 //
 // Packed layout of one matrix (built on the host by pack_eo, kept in the kernel
-// parameter space = constant bank, so every coefficient is a c[0x0][imm] DFMA
-// operand):
+// parameter space = constant bank; on sm_100a the compiler brings each coefficient pair
+// into uniform registers with one LDCU.128 and feeds DFMA from there, so the *_R variants
+// below apply every loaded coefficient to R lines):
 //   E[h][h]  (A[i][j] + A[i][n-1-j]) / 2,   i, j < h = n/2
 //   O[h][h]  (A[i][j] - A[i][n-1-j]) / 2
 //   C[h]     A[i][mid]                       (odd n: middle column)
@@ -108,6 +109,133 @@ __device__ __forceinline__ void eo_mul2(const T* __restrict__ A1, const EOSplit<
       ym = fma(R2[j], (S > 0) ? s2.e[j] : s2.o[j], ym);
     }
     y[H] = ym;
+  }
+}
+
+// R lines at once: every coefficient is loaded once and applied to the R lines (the
+// per-line accumulation order is that of eo_mul, so the results are bitwise identical)
+template <int N, int S, bool ACC, int R, typename T>
+__device__ __forceinline__ void eo_mul_R(const T* __restrict__ A, const EOSplit<N, T> (&s)[R], T (&y)[R][N]) {
+  constexpr int H = N / 2;
+  const T* E = A;
+  const T* O = A + H * H;
+  const T* C = A + 2 * H * H;
+  const T* Rw = A + 2 * H * H + H;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    T ye[R], yo[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      ye[r] = T(0);
+      yo[r] = T(0);
+    }
+    if (N & 1) {
+      const T c = C[i];
+#pragma unroll
+      for (int r = 0; r < R; ++r) ye[r] = c * s[r].m;
+    }
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      const T e = E[i * H + j], o = O[i * H + j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ye[r] = fma(e, s[r].e[j], ye[r]);
+        yo[r] = fma(o, s[r].o[j], yo[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const T lo = ye[r] + yo[r];
+      const T hi = (S > 0) ? (ye[r] - yo[r]) : (yo[r] - ye[r]);
+      if (ACC) {
+        y[r][i] += lo;
+        y[r][N - 1 - i] += hi;
+      } else {
+        y[r][i] = lo;
+        y[r][N - 1 - i] = hi;
+      }
+    }
+  }
+  if (N & 1) {
+    T ym[R];
+    const T cm = Rw[H];
+#pragma unroll
+    for (int r = 0; r < R; ++r) ym[r] = (S > 0) ? cm * s[r].m : T(0);
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      const T c = Rw[j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) ym[r] = fma(c, (S > 0) ? s[r].e[j] : s[r].o[j], ym[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (ACC)
+        y[r][H] += ym[r];
+      else
+        y[r][H] = ym[r];
+    }
+  }
+}
+
+// y = A1 x1 + A2 x2 for R lines (accumulation order of eo_mul2)
+template <int N, int S, int R, typename T>
+__device__ __forceinline__ void eo_mul2_R(const T* __restrict__ A1, const EOSplit<N, T> (&s1)[R],
+                                          const T* __restrict__ A2, const EOSplit<N, T> (&s2)[R], T (&y)[R][N]) {
+  constexpr int H = N / 2;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    T ye[R], yo[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      ye[r] = T(0);
+      yo[r] = T(0);
+    }
+    if (N & 1) {
+      const T c1 = A1[2 * H * H + i], c2 = A2[2 * H * H + i];
+#pragma unroll
+      for (int r = 0; r < R; ++r) ye[r] = fma(c2, s2[r].m, c1 * s1[r].m);
+    }
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      const T e = A1[i * H + j], o = A1[H * H + i * H + j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ye[r] = fma(e, s1[r].e[j], ye[r]);
+        yo[r] = fma(o, s1[r].o[j], yo[r]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      const T e = A2[i * H + j], o = A2[H * H + i * H + j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ye[r] = fma(e, s2[r].e[j], ye[r]);
+        yo[r] = fma(o, s2[r].o[j], yo[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      y[r][i] = ye[r] + yo[r];
+      y[r][N - 1 - i] = (S > 0) ? (ye[r] - yo[r]) : (yo[r] - ye[r]);
+    }
+  }
+  if (N & 1) {
+    const T* R1 = A1 + 2 * H * H + H;
+    const T* R2 = A2 + 2 * H * H + H;
+    T ym[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) ym[r] = (S > 0) ? fma(R2[H], s2[r].m, R1[H] * s1[r].m) : T(0);
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      const T c1 = R1[j], c2 = R2[j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ym[r] = fma(c1, (S > 0) ? s1[r].e[j] : s1[r].o[j], ym[r]);
+        ym[r] = fma(c2, (S > 0) ? s2[r].e[j] : s2[r].o[j], ym[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) y[r][H] = ym[r];
   }
 }
 

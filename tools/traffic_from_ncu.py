@@ -1,8 +1,9 @@
-"""Build profiles/r1_traffic.json from an ncu CSV of the C4 bench command:
+"""Build profiles/rN_traffic.json from an ncu CSV of the C4 bench command:
 
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-      --kernel-name-base demangled -k regex:k_kron4 --csv \
+      --kernel-name-base demangled -k regex:k_kron --csv \
       python bench.py --steps 1 --warmup 0 --quick > traffic.csv
+  python tools/traffic_from_ncu.py traffic.csv profiles/rN_traffic.json profiles/rN_traffic_ncu.csv
 
 Per degree p (template n = p+1) and mode (0 = APPLY, 1 = CHEBY_GL) the median DRAM
 bytes per launch are recorded next to the algorithmic bytes (16 / 40 B per DoF).
@@ -28,19 +29,26 @@ idi = hdr.index("ID")
 per = {}
 for r in rows:
     m = re.search(r"k_kron4<(?:\(int\))?(\d), (?:\(int\))?(\d), (?:\(int\))?(\d)", r[ki])
-    if not m:
+    m6 = re.search(r"k_kron6<(?:\(int\))?(\d), (?:\(int\))?(\d)", r[ki])
+    if m:
+        n, nl, mode = map(int, m.groups())
+        kern = "k_kron4"
+    elif m6:
+        n, mode = map(int, m6.groups())
+        nl, kern = 2, "k_kron6"
+    else:
         continue
-    n, nl, mode = map(int, m.groups())
     if nl != 2 or mode not in (0, 1):
         continue
-    key = (n - 1, mode)
+    key = (n - 1, mode, kern)
     per.setdefault(key, {}).setdefault(r[idi], {})[r[mi]] = float(r[vi].replace(",", ""))
 out = {"c4": {}}
-for (p, mode), launches in sorted(per.items()):
+src = sys.argv[3] if len(sys.argv) > 3 else sys.argv[1]
+for (p, mode, kern), launches in sorted(per.items()):
     tot = [v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in launches.values()]
-    name = "k_kron4<APPLY>" if mode == 0 else "k_kron4<CHEBY_GL>"
+    name = f"{kern}<APPLY>" if mode == 0 else f"{kern}<CHEBY_GL>"
     ent = out["c4"].setdefault(name, {"per_launch_bytes": {}, "algorithmic_bytes": {}, "launches": {},
-                                      "source": "profiles/r1_traffic_ncu.csv"})
+                                      "source": src})
     nd = c4_spec(p).n_dofs
     ent["per_launch_bytes"][str(p)] = statistics.median(tot)
     ent["algorithmic_bytes"][str(p)] = nd * (16.0 if mode == 0 else 40.0)
