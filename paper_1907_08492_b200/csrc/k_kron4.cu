@@ -68,8 +68,14 @@ template <> struct K4C<3> { static constexpr int R = 1, CPB = 32, CPBS = 20, TP 
 template <> struct K4C<4> { static constexpr int R = 2, CPB = 30, CPBS = 18, TP = 0, XSW = 0; static constexpr Lay3 ZY{4, 20, 88}, YX{5, 20, 88}, XZ{5, 20, 84}; };
 template <> struct K4C<5> { static constexpr int R = 2, CPB = 16, CPBS = 11, TP = 0, XSW = 0; static constexpr Lay3 ZY{5, 26, 143}, YX{5, 25, 134}, XZ{5, 25, 139}; };
 template <> struct K4C<6> { static constexpr int R = 1, CPB = 8, CPBS = 5, TP = 0, XSW = 0; static constexpr Lay3 ZY{6, 38, 228}, YX{9, 54, 324}, XZ{11, 66, 402}; };
+// n = 7 default since round 2 (DG_K4_ALT7, default 2): 32 threads per cell (4 idle), ZY and XZ conflict free
+template <> struct K4C<7, 2> { static constexpr int R = 2, CPB = 10, CPBS = 4, TP = 32, XSW = 0; static constexpr Lay3 ZY{7, 55, 385}, YX{7, 56, 392}, XZ{7, 49, 343}; };
 template <> struct K4C<7> { static constexpr int R = 2, CPB = 10, CPBS = 4, TP = 0, XSW = 0; static constexpr Lay3 ZY{7, 55, 396}, YX{7, 56, 392}, XZ{7, 49, 344}; };
 template <> struct K4C<8> { static constexpr int R = 1, CPB = 4, CPBS = 3, TP = 0, XSW = 0; static constexpr Lay3 ZY{8, 72, 576}, YX{9, 72, 576}, XZ{12, 97, 776}; };
+// n = 9 alternate (DG_K4_ALT9=2): the y->x layout padded to a row pitch of 17 (conflict free;
+// the default YX{9,85,765} costs 1.94x in the half-warp model).  Measured slower (C4 p=8:
+// matvec 139.8 -> 131.6, Chebyshev 87.1 -> 78.0 GDoF/s: 1.7x the shared memory per cell)
+template <> struct K4C<9, 2> { static constexpr int R = 1, CPB = 3, CPBS = 2, TP = 0, XSW = 0; static constexpr Lay3 ZY{9, 89, 801}, YX{17, 153, 1377}, XZ{9, 81, 729}; };
 template <> struct K4C<9> { static constexpr int R = 1, CPB = 3, CPBS = 2, TP = 0, XSW = 0; static constexpr Lay3 ZY{9, 89, 801}, YX{9, 85, 765}, XZ{9, 81, 729}; };
 // alternates (DG_K4_ALT=1): two lines per thread
 template <> struct K4C<6, 1> { static constexpr int R = 2, CPB = 16, CPBS = 8, TP = 0, XSW = 0; static constexpr Lay3 ZY{6, 38, 242}, YX{9, 54, 338}, XZ{6, 36, 217}; };
@@ -78,6 +84,9 @@ template <> struct K4C<8, 1> { static constexpr int R = 2, CPB = 8, CPBS = 4, TP
 // and the x stage maps thread (a, b) to line (j, k) = (b + r NB, a); with these the Y/X
 // transposes are bank-conflict free (tools/smem_layout_search7.py / smem_ktable_search.py)
 template <> struct K4C<5, 1> { static constexpr int R = 2, CPB = 16, CPBS = 11, TP = 16, XSW = 1; static constexpr Lay3 ZY{5, 27, 135}, YX{7, 37, 185}, XZ{5, 31, 155}; };
+// n = 5 default since round 2 (DG_K4_ALT5, default 2): 16 threads per cell without the x-stage swap
+// (coalesced x-line accesses), ZY and XZ conflict free, YX 1.5x (tools/k4_tp_layout_search.py 5 2 16 16 0)
+template <> struct K4C<5, 2> { static constexpr int R = 2, CPB = 16, CPBS = 11, TP = 16, XSW = 0; static constexpr Lay3 ZY{5, 27, 135}, YX{5, 25, 125}, XZ{5, 25, 125}; };
 // n = 3 alternate: 12 threads per cell (3 idle: they take block jobs) so that all three
 // transposes are bank-conflict free (the unpadded y->x layout costs 2x; ncu: 25 % of the
 // Chebyshev step's shared wavefronts were conflicts, LSU pipe 87 %)
@@ -1022,6 +1031,51 @@ cudaError_t launch_mode(int mode, const KronParamsT<Real>& kp, const GridArgs& g
     const char* e = std::getenv("DG_K4_ALT");
     return e ? std::atoi(e) : 0;
   }();
+  if constexpr (N == 5) {   // default: the unswapped padded configuration K4C<5, 2> (DG_K4_ALT5=0: K4C<5>)
+    static const int alt5 = [] {
+      const char* e = std::getenv("DG_K4_ALT5");
+      return e ? std::atoi(e) : 2;   // measured (C4 p=4): matvec 120 -> 132, Chebyshev step 75.6 -> 81.1 GDoF/s
+    }();
+    if (alt5 == 2) {
+      switch (mode) {
+        case KMODE_APPLY: return launch_t<N, NL, KMODE_APPLY, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 2, Real>(kp, g, u, y, ch, s);
+      }
+      return cudaErrorInvalidValue;
+    }
+  }
+  if constexpr (N == 7) {   // default: the padded configuration K4C<7, 2> (DG_K4_ALT7=0: K4C<7>)
+    static const int alt7 = [] {
+      const char* e = std::getenv("DG_K4_ALT7");
+      return e ? std::atoi(e) : 2;   // measured (C4 p=6): matvec 118.6 -> 125.9, Chebyshev 72.2 -> 74.6 GDoF/s
+    }();
+    if (alt7 == 2) {
+      switch (mode) {
+        case KMODE_APPLY: return launch_t<N, NL, KMODE_APPLY, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 2, Real>(kp, g, u, y, ch, s);
+      }
+      return cudaErrorInvalidValue;
+    }
+  }
+  if constexpr (N == 9) {   // DG_K4_ALT9=2: the padded-YX alternate K4C<9, 2> (A/B)
+    static const int alt9 = [] {
+      const char* e = std::getenv("DG_K4_ALT9");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (alt9 == 2) {
+      switch (mode) {
+        case KMODE_APPLY: return launch_t<N, NL, KMODE_APPLY, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 2, Real>(kp, g, u, y, ch, s);
+      }
+      return cudaErrorInvalidValue;
+    }
+  }
   if constexpr (K4HasAlt<N>::value) {
     if ((alt_mask >> (N - 3)) & 1) {
       switch (mode) {

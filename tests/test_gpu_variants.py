@@ -18,6 +18,8 @@ VARIANTS = [
     ({"DG_QUAD": "1"}, "3", True),
     ({"DG_K4_ALT": "44"}, "4,5,7", False),   # alternates at n = 5, 6, 8 (bits n-3)
     ({"DG_K4_ALT": "1"}, "2", False),        # n = 3 alternate (padded threads)
+    ({"DG_K4_ALT5": "0"}, "4", False),       # n = 5: round 1's unpadded configuration
+    ({"DG_K4_ALT7": "0"}, "6", False),       # n = 7: round 1's unpadded configuration
     ({"DG_K4_OUT": "0"}, "3,5", False),
     ({"DG_K4_OUT": "1"}, "2,4", False),
     ({"DG_BCHG": "4"}, "1,3,4,5,6,7", False),
