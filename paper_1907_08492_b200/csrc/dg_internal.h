@@ -94,9 +94,18 @@ struct QuadParams {
 
 enum { GEOM_CONST = 0, GEOM_PER_CELL = 1, GEOM_PER_QPOINT = 2 };
 
+// Index of quadrature point (q0, q1, q2) (x, y, z) inside one [n^3] block of the per-q-point
+// merged tensor: x slowest, then z, then y, so that the x-line threads (one per (q1, q2)) of
+// the quadrature kernels read consecutive addresses at each position q0 along their line
+// (coalesced 64-bit loads instead of per-thread runs of n).
+template <int N>
+__host__ __device__ __forceinline__ int gq(int q0, int q1, int q2) {
+  return (q0 * N + q2) * N + q1;
+}
+
 // Geometry arrays of the general path (device pointers, library-owned).
 struct GeomArgs {
-  const double* G;             // PER_QPOINT: [cell][6][n^3]  w_q det J J^-1 J^-T
+  const double* G;             // PER_QPOINT: [cell][6][n^3 in gq order]  w_q det J J^-1 J^-T
   const double* face[3];       // PER_QPOINT: per direction [face][4][n^2]: dA J^-1 n_+ (3), sigma dA
   const double* jinv;          // PER_CELL:  [cell][10]: J^-1 (row-major), det J
   double pen;                  // (p+1)^2 * penalty_factor  (PER_CELL)

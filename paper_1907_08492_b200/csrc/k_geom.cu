@@ -100,7 +100,7 @@ __global__ void k_geom_cells(const MapParams mp, int Nx, int Ny, int nz, double*
     const double det = inv3(J, Ji);
     if (!(det > 0.0) || !isfinite(det)) atomicOr(err, 1);
     const double w = mp.wq[q0] * mp.wq[q1] * mp.wq[q2] * det;
-    double* g = G + cell * (6 * N3) + q;
+    double* g = G + cell * (6 * N3) + gq<N>(q0, q1, q2);
     // (a,b) = sum_k Ji[a][k] Ji[b][k]
     g[0 * N3] = w * (Ji[0] * Ji[0] + Ji[1] * Ji[1] + Ji[2] * Ji[2]);
     g[1 * N3] = w * (Ji[3] * Ji[3] + Ji[4] * Ji[4] + Ji[5] * Ji[5]);

@@ -395,7 +395,7 @@ k_quad(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs g
     for (int k = 0; k < N; ++k) {
       double G[6];
       if constexpr (GEOM == GEOM_PER_QPOINT) {
-        const double* gp = ga.G + cid * (int64_t)(6 * N * NN) + k * NN + j * N + i;
+        const double* gp = ga.G + cid * (int64_t)(6 * N * NN) + gq<N>(i, j, k);
 #pragma unroll
         for (int q = 0; q < 6; ++q) G[q] = __ldg(gp + q * N * NN);
       } else {
@@ -628,7 +628,7 @@ __global__ void k_diag_general(const __grid_constant__ DiagTables t, const __gri
       const double g2 = s0 * s1 * t.DS[q2 * N + ii[2]];
       double G[6];
       if constexpr (GEOM == GEOM_PER_QPOINT) {
-        for (int m = 0; m < 6; ++m) G[m] = ga.G[cid * (6 * N3) + m * N3 + q];
+        for (int m = 0; m < 6; ++m) G[m] = ga.G[cid * (6 * N3) + m * N3 + gq<N>(q0, q1, q2)];
       } else {
         const double w = qp.w[q0] * qp.w[q1] * qp.w[q2];
         for (int m = 0; m < 6; ++m) G[m] = w * Gc[m];

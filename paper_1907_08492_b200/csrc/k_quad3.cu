@@ -474,23 +474,14 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
       eo_apply<N, -1>(qp.D, c1, gx);
       eo_apply<N, 1>(qp.S, c2, gy);
       eo_apply<N, 1>(qp.S, c3, gz);
-      const double* Gp = ga.G + cid * (6 * N3) + (xq2 * N + xq1) * N;
+      const double* Gp = ga.G + cid * (6 * N3) + gq<N>(0, xq1, xq2);
       const double wyz = qp.w[xq1] * qp.w[xq2];
       double Gl[GEOM == GEOM_PER_QPOINT ? 6 : 1][N];
-      if constexpr (GEOM == GEOM_PER_QPOINT) {   // the x-line's tensors: contiguous runs of n
-#pragma unroll
+      if constexpr (GEOM == GEOM_PER_QPOINT) {   // the x-line's tensors: consecutive lines are
+#pragma unroll                                     // consecutive addresses at every position k (gq)
         for (int m = 0; m < 6; ++m) {
-          if constexpr (N % 2 == 0) {
 #pragma unroll
-            for (int k = 0; k < N; k += 2) {
-              const double2 v = __ldg(reinterpret_cast<const double2*>(Gp + m * N3 + k));
-              Gl[m][k] = v.x;
-              Gl[m][k + 1] = v.y;
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < N; ++k) Gl[m][k] = __ldg(Gp + m * N3 + k);
-          }
+          for (int k = 0; k < N; ++k) Gl[m][k] = __ldg(Gp + m * N3 + k * N * N);
         }
       }
 #pragma unroll
