@@ -11,12 +11,12 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1907_08492_b200 as P  # noqa: E402
-from synthetic import c4_spec  # noqa: E402
+from synthetic import CONFIGS, c4_spec  # noqa: E402
 
-p = int(sys.argv[1])
+p = sys.argv[1]   # a C4 degree, or a BASELINE config name (C2, C3, C5)
 ops = (sys.argv[2] if len(sys.argv) > 2 else "apply,bchg,cheby").split(",")
 rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 2
-spec = c4_spec(p)
+spec = CONFIGS[p] if p in CONFIGS else c4_spec(int(p))
 m = P.mesh_from_spec(spec)
 g = torch.Generator(device="cuda").manual_seed(1)
 u = torch.rand(m.n_local_dofs, dtype=torch.float64, device="cuda", generator=g)
