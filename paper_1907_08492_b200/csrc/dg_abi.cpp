@@ -274,6 +274,15 @@ bool kron6_use(int n, int NL, int mode) {
   return kron6_supported(n, NL, mode) && ((mask >> bit) & 1);
 }
 
+// n = 3 cell-per-thread kernel k_kron3c (DG_K3C=0 falls back to k_kron6 / k_kron4)
+bool kron3c_use(int n, int NL) {
+  static const int v = [] {
+    const char* e = std::getenv("DG_K3C");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0 && kron3c_supported(n, NL);
+}
+
 // general kernel selection: k_quad3 (z-first) unless DG_QUAD=1 asks for k_quad.cu
 bool quad_v3(int n, int geom) {
   static const int v = [] {
@@ -1128,7 +1137,9 @@ dg_status run_pass(dg_mesh m, int mode, bool kron, const double* u, double* y, c
     if (ze <= zb) return DG_OK;
     GridArgs g = grid_args(m, zb, ze);
     cudaError_t e;
-    if (kron && kron6_use(m->n, m->NL, mode))
+    if (kron && kron3c_use(m->n, m->NL))
+      e = launch_kron3c(m->NL, mode, m->kp, g, u, y, ch, s);
+    else if (kron && kron6_use(m->n, m->NL, mode))
       e = launch_kron6(m->n, mode, m->kp, g, u, y, ch, s);
     else if (kron && kron_v4(m->n))
       e = launch_kron4(m->n, m->NL, mode, m->kp, g, u, y, ch, s);
@@ -1566,7 +1577,9 @@ dg_status launch_apply_range(dg_mesh m, bool kron, const double* u, double* y, i
   GridArgs g = grid_args(m, zb, ze);
   ChebyArgs ch{};
   cudaError_t e;
-  if (kron && kron6_use(m->n, m->NL, KMODE_APPLY))
+  if (kron && kron3c_use(m->n, m->NL))
+    e = launch_kron3c(m->NL, KMODE_APPLY, m->kp, g, u, y, ch, s);
+  else if (kron && kron6_use(m->n, m->NL, KMODE_APPLY))
     e = launch_kron6(m->n, KMODE_APPLY, m->kp, g, u, y, ch, s);
   else if (kron && kron_v4(m->n))
     e = launch_kron4(m->n, m->NL, KMODE_APPLY, m->kp, g, u, y, ch, s);

@@ -129,6 +129,10 @@ struct MapParams {
 bool kron4_supported(int n);
 cudaError_t launch_kron4(int n, int NL, int mode, const KronParams& kp, const GridArgs& g,
                          const double* u, double* y, const ChebyArgs& ch, cudaStream_t s);
+// n = 3 cell-per-thread Cartesian kernel (k_kron3c.cu): matvec and every fused Chebyshev mode
+bool kron3c_supported(int n, int NL);
+cudaError_t launch_kron3c(int NL, int mode, const KronParams& kp, const GridArgs& g, const double* u, double* y,
+                          const ChebyArgs& ch, cudaStream_t s);
 // i-plane Cartesian matvec (k_kron6.cu): z and y sweeps of a whole (j,k) plane per thread
 bool kron6_supported(int n, int NL, int mode);
 cudaError_t launch_kron6(int n, int mode, const KronParams& kp, const GridArgs& g, const double* u, double* y,

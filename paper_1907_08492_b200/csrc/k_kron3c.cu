@@ -1,0 +1,447 @@
+// Cartesian fast path at n = 3 (p = 2): one thread per cell (k_kron3c).
+//
+// Same operator as k_kron4 — the Kronecker form of Eq. (14) with the
+// neighbour couplings N^{+-} on the NL layers next to each face — and the
+// same fused Chebyshev step (Eqs. (11)-(12)).  At n = 3 a
+// cell has 27 DoF, so a thread keeps the whole cell in registers: every 1D sweep of every
+// direction runs in registers with the coefficients amortised over the cell's 9 lines, and no
+// shared-memory transposes or block barriers are needed (k_kron4 at n = 3 spends ~120 of its
+// 270 instructions per DoF on index/control work and runs its LSU pipe at 87 %).
+//
+// A warp owns a tile of up to 32 consecutive cells of one x-row (lane = cell).  Global data
+// moves through per-warp shared-memory slots filled by cp.async with coalesced addresses
+// (lane l copies elements l, l+32, ... of the contiguous tile) and read back per cell with
+// stride 27 doubles (conflict free).  Neighbours:
+//   z: the tile of the plane above / below (or the slab halo, or the mirror ghost);
+//   y: the tile of the row above / below -> M_z on its NL layers (the y-ghost of k_kron4);
+//   x: the c = M_y M_z u field of the adjacent lane by warp shuffle; at the tile edges the
+//      x-neighbour's NL layers are swept by 2*NL*3 helper lanes (z then y), or mirrored.
+// Slot schedule (4 slots, cp.async groups):
+//   u -> S0, z- -> S1, z+ -> S2, y- -> S3;  Z stage;  y+ -> S0 (b -> S1, dinv -> S2);
+//   Y, X stages;  (residual; u -> S3, u_prev -> S0;  P^-1 x, y;  z with dinv;  y, x; update)
+//   result staged in S1 and stored with coalesced addresses.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "dg_internal.h"
+#include "fdm.cuh"
+
+namespace dgb {
+namespace {
+
+constexpr int N = 3, NN = 9, N3 = 27, TW = 32, NSLOT = 4;
+
+__device__ __forceinline__ int ix(int i, int j, int k) { return k * NN + j * N + i; }
+
+__device__ __forceinline__ void cpa8(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa16(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
+}
+
+// warp-cooperative copy of cnt contiguous doubles into a slot (16-byte copies when both ends
+// are 16-byte aligned; the slot bases are), then one commit (an empty group if src == nullptr)
+__device__ __forceinline__ void tile_load(double* dst, const double* src, int cnt, int lane) {
+  if (src) {
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+      const int c2 = cnt >> 1;
+      for (int e = lane; e < c2; e += 32) cpa16(dst + 2 * e, src + 2 * e);
+      if ((cnt & 1) && lane == 0) cpa8(dst + cnt - 1, src + cnt - 1);
+    } else {
+      for (int e = lane; e < cnt; e += 32) cpa8(dst + e, src + e);
+    }
+  }
+  cpa_commit();
+}
+
+template <int NL, int MODE>
+__global__ void __launch_bounds__(TW) k_kron3c(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g,
+                                               const double* __restrict__ u, double* __restrict__ y,
+                                               const __grid_constant__ ChebyArgs ch) {
+  __shared__ __align__(16) double S[NSLOT][TW * N3];
+  __shared__ double EXT[2][NL][N][N];   // edge helpers: (M_z u_{x+-})[l][j'][k] at the NL i-layers
+  __shared__ double EX[2][NL][N][N];    // edge helpers: c_{x+-} = (M_y M_z u_{x+-})[l][j][k]
+
+  const int lane = threadIdx.x;
+  const int cx0 = blockIdx.x * TW, cy = blockIdx.y, cz = g.zbeg + blockIdx.z;
+  const int ncell = g.Nx - cx0 < TW ? g.Nx - cx0 : TW;
+  const bool active = lane < ncell;
+  const int64_t plane = (int64_t)g.Nx * g.Ny;
+  const int64_t rowcell = ((int64_t)cz * g.Ny + cy) * g.Nx;
+  const int64_t c0 = rowcell + cx0;   // first cell of the tile
+  const int tcnt = ncell * N3;
+
+  // x-neighbour sources of the tile edges (cell index in the row, or -1: mirror)
+  const bool xper = g.bc[0] == DG_BC_PERIODIC;
+  const int h0 = cx0 > 0 ? cx0 - 1 : (xper ? g.Nx - 1 : -1);
+  const int h1 = cx0 + ncell < g.Nx ? cx0 + ncell : (xper ? 0 : -1);
+  // y-neighbour rows (-1: mirror)
+  const bool yper = g.bc[1] == DG_BC_PERIODIC;
+  const int ym_row = cy > 0 ? cy - 1 : (yper ? g.Ny - 1 : -1);
+  const int yp_row = cy + 1 < g.Ny ? cy + 1 : (yper ? 0 : -1);
+  // z-neighbour tiles: source, cell stride (own layout 27, halo NL*9), layer offset
+  const double* zsrc[2];
+  int zcs[2], zoff[2];
+  bool zmir[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int nz = cz + (s ? 1 : -1);
+    zcs[s] = N3;
+    zoff[s] = 0;
+    zmir[s] = false;
+    if (nz >= 0 && nz < g.nz) {
+      zsrc[s] = u + (c0 + (s ? plane : -plane)) * N3;
+    } else {
+      const int src = s ? g.zhi : g.zlo;
+      if (src == ZSRC_MIRROR) {
+        zsrc[s] = nullptr;
+        zmir[s] = true;
+      } else if (src == ZSRC_LOCAL) {   // periodic wrap inside the slab
+        zsrc[s] = u + (c0 + (s ? -(int64_t)(g.nz - 1) : (int64_t)(g.nz - 1)) * plane) * N3;
+      } else {                          // slab halo: [cell][NL][n][n]
+        zsrc[s] = (s ? g.halo_hi : g.halo_lo) + ((int64_t)cy * g.Nx + cx0) * (NL * NN);
+        zcs[s] = NL * NN;
+        zoff[s] = s ? 0 : (N - NL) * NN;
+      }
+    }
+  }
+
+  // ---- stage 0: issue the tile copies of the Z and Y stages
+  tile_load(S[0], u + c0 * N3, tcnt, lane);
+  tile_load(S[1], zsrc[0], ncell * zcs[0], lane);
+  tile_load(S[2], zsrc[1], ncell * zcs[1], lane);
+  tile_load(S[3], ym_row >= 0 ? u + (((int64_t)cz * g.Ny + ym_row) * g.Nx + cx0) * N3 : nullptr, tcnt, lane);
+  // edge helpers (lanes < 2*NL*N): z-line (l, j') of the NL i-layers of the x-neighbour
+  constexpr int NEDGE = 2 * NL * N;
+  const int es = lane / (NL * N), erem = lane - es * (NL * N), el = erem / N, ejk = erem - el * N;
+  const int eh = es ? h1 : h0;
+  const bool edge = lane < NEDGE && eh >= 0;
+  double eu[N];
+  if (edge) {
+    const int ei = es ? el : N - NL + el;
+    const double* src = u + (rowcell + eh) * N3 + ejk * N + ei;
+#pragma unroll
+    for (int k = 0; k < N; ++k) eu[k] = __ldg(src + k * NN);
+  }
+
+  cpa_wait<1>();   // u, z-, z+ landed (y- may be in flight)
+  __syncwarp();
+
+  // ---- Z: t = M_z u, a = L_z u + N_z^{+-} u_{z+-}
+  double t[N3], a[N3];
+  if (active) {
+    const double* us = S[0] + lane * N3;
+    const double* zm_t = S[1] + lane * zcs[0] - zoff[0];
+    const double* zp_t = S[2] + lane * zcs[1] - zoff[1];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double uz[N], zm[NL], zp[NL], tl[N], al[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) uz[k] = us[ix(i, j, k)];
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          const int Lm = N - NL + l, Lp = l;
+          zm[l] = zmir[0] ? -uz[N - 1 - Lm] : zm_t[ix(i, j, Lm)];
+          zp[l] = zmir[1] ? -uz[N - 1 - Lp] : zp_t[ix(i, j, Lp)];
+        }
+        const auto su = eo_split<N>(uz);
+        eo_mul<N, 1, false>(kp.M, su, tl);
+        eo_mul<N, 1, false>(kp.L[2], su, al);
+        dense_add<NL, NL>(kp.Nm[2], zm, &al[0]);
+        dense_add<NL, NL>(kp.Np[2], zp, &al[N - NL]);
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          t[ix(i, j, k)] = tl[k];
+          a[ix(i, j, k)] = al[k];
+        }
+      }
+    }
+  }
+  if (edge) {
+    double o[N];
+    eo_apply<N, 1>(kp.M, eu, o);
+#pragma unroll
+    for (int k = 0; k < N; ++k) EXT[es][el][ejk][k] = o[k];
+  }
+  __syncwarp();   // S0..S2 read, EXT written
+
+  // ---- issue the next copies: y+ (and the Chebyshev b, dinv)
+  tile_load(S[0], yp_row >= 0 ? u + (((int64_t)cz * g.Ny + yp_row) * g.Nx + cx0) * N3 : nullptr, tcnt, lane);
+  if constexpr (MODE != KMODE_APPLY) {
+    tile_load(S[1], ch.b + c0 * N3, tcnt, lane);
+    tile_load(S[2], MODE == KMODE_CHEBY_FDM ? nullptr : ch.dinv + c0 * N3, tcnt, lane);
+    cpa_wait<2>();   // y-, y+ landed
+  } else {
+    cpa_wait<0>();
+  }
+  __syncwarp();
+
+  // ---- Y: b = M_y a + L_y t + N_y^{+-} (M_z u_{y+-}),  c = M_y t   (in place: a <- b, t <- c)
+  if (edge) {   // edge helpers: y-sweep of EXT -> EX
+    double v[N], o[N];
+#pragma unroll
+    for (int jp = 0; jp < N; ++jp) v[jp] = EXT[es][el][jp][ejk];   // ejk = k here
+    eo_apply<N, 1>(kp.M, v, o);
+#pragma unroll
+    for (int j = 0; j < N; ++j) EX[es][el][j][ejk] = o[j];
+  }
+  if (active) {
+    const double* ym_t = S[3] + lane * N3;
+    const double* yp_t = S[0] + lane * N3;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      // y-ghosts of this i: (M_z u_{y+-}) at the neighbours' NL layers, [l][k]
+      double gym[NL][N], gyp[NL][N];
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        if (ym_row >= 0) {
+          double v[N];
+#pragma unroll
+          for (int k = 0; k < N; ++k) v[k] = ym_t[ix(i, N - NL + l, k)];
+          eo_apply<N, 1>(kp.M, v, gym[l]);
+        }
+        if (yp_row >= 0) {
+          double v[N];
+#pragma unroll
+          for (int k = 0; k < N; ++k) v[k] = yp_t[ix(i, l, k)];
+          eo_apply<N, 1>(kp.M, v, gyp[l]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double al[N], tl[N], bl[N], cl[N], gm[NL], gp[NL];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          al[j] = a[ix(i, j, k)];
+          tl[j] = t[ix(i, j, k)];
+        }
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          gm[l] = ym_row >= 0 ? gym[l][k] : -tl[NL - 1 - l];
+          gp[l] = yp_row >= 0 ? gyp[l][k] : -tl[N - 1 - l];
+        }
+        const auto st = eo_split<N>(tl);
+        eo_mul2<N, 1>(kp.M, eo_split<N>(al), kp.L[1], st, bl);
+        eo_mul<N, 1, false>(kp.M, st, cl);
+        dense_add<NL, NL>(kp.Nm[1], gm, &bl[0]);
+        dense_add<NL, NL>(kp.Np[1], gp, &bl[N - NL]);
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          a[ix(i, j, k)] = bl[j];
+          t[ix(i, j, k)] = cl[j];
+        }
+      }
+    }
+  }
+  __syncwarp();   // EX written, S3 / S0 (y tiles) read
+
+  // ---- X: y = M_x b + L_x c + N_x^{+-} c_{x+-}   (c of the adjacent lanes by shuffle)
+  const unsigned full = 0xffffffffu;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double bl[N], cl[N], res[N], cxm[NL], cxp[NL];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        bl[i] = a[ix(i, j, k)];
+        cl[i] = t[ix(i, j, k)];
+      }
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        const int Lm = N - NL + l, Lp = l;
+        const double vm = __shfl_up_sync(full, cl[Lm], 1);
+        const double vp = __shfl_down_sync(full, cl[Lp], 1);
+        cxm[l] = lane > 0 ? vm : (h0 >= 0 ? EX[0][l][j][k] : -cl[N - 1 - Lm]);
+        cxp[l] = lane + 1 < ncell ? vp : (h1 >= 0 ? EX[1][l][j][k] : -cl[N - 1 - Lp]);
+      }
+      eo_mul2<N, 1>(kp.M, eo_split<N>(bl), kp.L[0], eo_split<N>(cl), res);
+      dense_add<NL, NL>(kp.Nm[0], cxm, &res[0]);
+      dense_add<NL, NL>(kp.Np[0], cxp, &res[N - NL]);
+#pragma unroll
+      for (int i = 0; i < N; ++i) a[ix(i, j, k)] = res[i];
+    }
+  }
+
+  if constexpr (MODE == KMODE_APPLY) {
+    double* O = S[1];
+    if (active) {
+#pragma unroll
+      for (int e = 0; e < N3; ++e) O[lane * N3 + e] = a[e];
+    }
+    __syncwarp();
+    double* yt = y + c0 * N3;
+    for (int e = lane; e < tcnt; e += 32) yt[e] = O[e];
+    return;
+  } else {
+    cpa_wait<1>();   // b landed (dinv may be in flight)
+    __syncwarp();
+    if (active) {   // r = b - A u
+      const double* bs = S[1] + lane * N3;
+#pragma unroll
+      for (int e = 0; e < N3; ++e) a[e] = bs[e] - a[e];
+    }
+    __syncwarp();   // S3 (y-), S0 (y+) and S1 (b) free
+    tile_load(S[3], u + c0 * N3, tcnt, lane);
+    tile_load(S[0], ch.first ? nullptr : ch.u_prev + c0 * N3, tcnt, lane);
+    double* z = a;   // P^{-1} r in place
+    if constexpr (MODE == KMODE_CHEBY_PJ) {
+      cpa_wait<2>();   // dinv
+      __syncwarp();
+      if (active) {
+        const double* ds = S[2] + lane * N3;
+#pragma unroll
+        for (int e = 0; e < N3; ++e) z[e] *= ds[e];
+      }
+    } else {
+      // x, y: T^{-T} (FDM: Z^T)
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          double v[N], o[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) v[i] = z[ix(i, j, k)];
+          if constexpr (MODE == KMODE_CHEBY_FDM) fdm_fwd<N>(kp, v, o);
+          else eo_apply<N, 1>(kp.TiT, v, o);
+#pragma unroll
+          for (int i = 0; i < N; ++i) z[ix(i, j, k)] = o[i];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double v[N], o[N];
+#pragma unroll
+          for (int j = 0; j < N; ++j) v[j] = z[ix(i, j, k)];
+          if constexpr (MODE == KMODE_CHEBY_FDM) fdm_fwd<N>(kp, v, o);
+          else eo_apply<N, 1>(kp.TiT, v, o);
+#pragma unroll
+          for (int j = 0; j < N; ++j) z[ix(i, j, k)] = o[j];
+        }
+      }
+      cpa_wait<2>();   // dinv
+      __syncwarp();
+      // z: T^{-T}, diag(A_GL)^{-1}, T^{-1}   (FDM: Z^T, 1/(sum_d c_d lam), Z)
+      const double* ds = S[2] + lane * N3;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double v[N], o[N];
+#pragma unroll
+          for (int k = 0; k < N; ++k) v[k] = z[ix(i, j, k)];
+          if constexpr (MODE == KMODE_CHEBY_FDM) {
+            fdm_fwd<N>(kp, v, o);
+            const double base = fma(kp.cdir[0], kp.lam[i], kp.cdir[1] * kp.lam[j]);
+#pragma unroll
+            for (int k = 0; k < N; ++k) o[k] /= fma(kp.cdir[2], kp.lam[k], base);
+            fdm_bwd<N>(kp, o, v);
+          } else {
+            eo_apply<N, 1>(kp.TiT, v, o);
+            if (active) {
+#pragma unroll
+              for (int k = 0; k < N; ++k) o[k] *= ds[ix(i, j, k)];
+            }
+            eo_apply<N, 1>(kp.Ti, o, v);
+          }
+#pragma unroll
+          for (int k = 0; k < N; ++k) z[ix(i, j, k)] = v[k];
+        }
+      }
+      // y, x: T^{-1} (FDM: Z)
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double v[N], o[N];
+#pragma unroll
+          for (int j = 0; j < N; ++j) v[j] = z[ix(i, j, k)];
+          if constexpr (MODE == KMODE_CHEBY_FDM) fdm_bwd<N>(kp, v, o);
+          else eo_apply<N, 1>(kp.Ti, v, o);
+#pragma unroll
+          for (int j = 0; j < N; ++j) z[ix(i, j, k)] = o[j];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          double v[N], o[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) v[i] = z[ix(i, j, k)];
+          if constexpr (MODE == KMODE_CHEBY_FDM) fdm_bwd<N>(kp, v, o);
+          else eo_apply<N, 1>(kp.Ti, v, o);
+#pragma unroll
+          for (int i = 0; i < N; ++i) z[ix(i, j, k)] = o[i];
+        }
+      }
+    }
+    cpa_wait<0>();   // u, u_prev
+    __syncwarp();
+    // three-term update, Eq. (11): u_{j+1} = u_j + c_prev (u_j - u_{j-1}) + c_z z
+    double* O = S[1];
+    if (active) {
+      const double* uj = S[3] + lane * N3;
+      const double* up = S[0] + lane * N3;
+#pragma unroll
+      for (int e = 0; e < N3; ++e) {
+        double v = fma(ch.c_z, z[e], uj[e]);
+        if (!ch.first) v = fma(ch.c_prev, uj[e] - up[e], v);
+        O[lane * N3 + e] = v;
+      }
+    }
+    __syncwarp();
+    double* ot = ch.u_next + c0 * N3;
+    for (int e = lane; e < tcnt; e += 32) ot[e] = O[e];
+  }
+}
+
+template <int NL, int MODE>
+cudaError_t launch_t(const KronParams& kp, const GridArgs& g, const double* u, double* y, const ChebyArgs& ch,
+                     cudaStream_t s) {
+  const int planes = g.zend - g.zbeg;
+  if (planes <= 0 || g.Nx <= 0 || g.Ny <= 0) return cudaSuccess;
+  if (g.Ny > 65535 || planes > 65535) return cudaErrorInvalidValue;
+  const dim3 grid((g.Nx + TW - 1) / TW, g.Ny, planes);
+  k_kron3c<NL, MODE><<<grid, TW, 0, s>>>(kp, g, u, y, ch);
+  return cudaGetLastError();
+}
+
+template <int NL>
+cudaError_t launch_mode(int mode, const KronParams& kp, const GridArgs& g, const double* u, double* y,
+                        const ChebyArgs& ch, cudaStream_t s) {
+  switch (mode) {
+    case KMODE_APPLY: return launch_t<NL, KMODE_APPLY>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_GL: return launch_t<NL, KMODE_CHEBY_GL>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_PJ: return launch_t<NL, KMODE_CHEBY_PJ>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_FDM: return launch_t<NL, KMODE_CHEBY_FDM>(kp, g, u, y, ch, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+bool kron3c_supported(int n, int NL) { return n == 3 && (NL == 2 || NL == 3); }
+
+cudaError_t launch_kron3c(int NL, int mode, const KronParams& kp, const GridArgs& g, const double* u, double* y,
+                          const ChebyArgs& ch, cudaStream_t s) {
+  if (NL == 2) return launch_mode<2>(mode, kp, g, u, y, ch, s);
+  if (NL == 3) return launch_mode<3>(mode, kp, g, u, y, ch, s);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dgb

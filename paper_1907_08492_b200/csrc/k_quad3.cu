@@ -42,6 +42,14 @@ struct Lay3 {
   int Pj, Pk, CS;
 };
 
+#ifndef Q3_GEARLY
+#define Q3_GEARLY 0     // 1: the X stage's per-q-point tensors (and x-face geometry) are loaded before the
+                        //    Y->X barrier, so their latency overlaps the barrier wait
+#endif
+#ifndef Q3_JOBPRE
+#define Q3_JOBPRE 0     // 1: the y/z-face jobs of stage X load their face geometry before their sweeps
+#endif
+
 // per n: cells per block and the two transposition layouts (ZY: z-write / y-read,
 // YX: y-write / x-read; the reverse transposes use the same two by symmetry)
 template <int N> struct Q3C;
@@ -410,10 +418,28 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
       st_line<N>(R3 + cslot * LYX.CS + at(LYX, yi, 0, yq), LYX.Pj, c3);
     }
   }
+  const int xq1 = ta, xq2 = tb;   // x-line (qy, qz)
+  constexpr bool kGE = Q3_GEARLY && GEOM == GEOM_PER_QPOINT;
+  double Gl[GEOM == GEOM_PER_QPOINT ? 6 : 1][N];
+  double xcv[kGE ? 2 : 1][3], xsd[kGE ? 2 : 1];
+  auto load_G = [&]() {
+    const double* Gp = ga.G + cid * (6 * N3) + gq<N>(0, xq1, xq2);
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) Gl[m][k] = __ldg(Gp + m * N3 + k * N * N);
+    }
+  };
+  if constexpr (kGE) {
+    if (active) {
+      load_G();
+#pragma unroll
+      for (int s = 0; s < 2; ++s) fgeom<N, GEOM>(qp, ga, g, cx, cy, cz, 0, s, xq1, xq2, xcv[s], xsd[s]);
+    }
+  }
   __syncthreads();
 
   // ================================================================ X (+ X^T)
-  const int xq1 = ta, xq2 = tb;   // x-line (qy, qz)
   {
     double q1[N], q2[N], q3[N];
     if (active) {
@@ -474,16 +500,9 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
       eo_apply<N, -1>(qp.D, c1, gx);
       eo_apply<N, 1>(qp.S, c2, gy);
       eo_apply<N, 1>(qp.S, c3, gz);
-      const double* Gp = ga.G + cid * (6 * N3) + gq<N>(0, xq1, xq2);
       const double wyz = qp.w[xq1] * qp.w[xq2];
-      double Gl[GEOM == GEOM_PER_QPOINT ? 6 : 1][N];
-      if constexpr (GEOM == GEOM_PER_QPOINT) {   // the x-line's tensors: consecutive lines are
-#pragma unroll                                     // consecutive addresses at every position k (gq)
-        for (int m = 0; m < 6; ++m) {
-#pragma unroll
-          for (int k = 0; k < N; ++k) Gl[m][k] = __ldg(Gp + m * N3 + k * N * N);
-        }
-      }
+      // the x-line's tensors: consecutive lines are consecutive addresses at every position k (gq)
+      if constexpr (GEOM == GEOM_PER_QPOINT && !kGE) load_G();
 #pragma unroll
       for (int k = 0; k < N; ++k) {
         double G[6];
@@ -509,7 +528,14 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         double cvec[3], sdA;
-        fgeom<N, GEOM>(qp, ga, g, cx, cy, cz, 0, s, xq1, xq2, cvec, sdA);
+        if constexpr (kGE) {
+          cvec[0] = xcv[s][0];
+          cvec[1] = xcv[s][1];
+          cvec[2] = xcv[s][2];
+          sdA = xsd[s];
+        } else {
+          fgeom<N, GEOM>(qp, ga, g, cx, cy, cz, 0, s, xq1, xq2, cvec, sdA);
+        }
         double rv, rn, ra, rb;
         flux(cvec, sdA, 0, xj[s], xsn[s], xsa[s], xsb[s], rv, rn, ra, rb);
 #pragma unroll
@@ -529,7 +555,13 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
         const int kind = jj / (2 * N);         // 0: y-face, 1: z-face
         const int s = (jj / N) & 1, q = jj % N;
         const int ccx = cx0 + c;
+        const int d = kind ? 2 : 1;
         const double* fin = FBb + c * Lay::FBC + (kind * 8 + s * 4) * FP + q * PG;
+        double jcv[Q3_JOBPRE ? N : 1][3], jsd[Q3_JOBPRE ? N : 1];
+        if constexpr (Q3_JOBPRE) {
+#pragma unroll
+          for (int qx = 0; qx < N; ++qx) fgeom<N, GEOM>(qp, ga, g, ccx, cy, cz, d, s, qx, q, jcv[qx], jsd[qx]);
+        }
         double J[N], Sa[N], Sb[N], Sd[N];
         {
           double v[N];
@@ -552,12 +584,15 @@ k_quad3(const __grid_constant__ QuadParams qp, const __grid_constant__ GeomArgs 
           }
         }
         double rv[N], rn[N], ra[N], rb[N];
-        const int d = kind ? 2 : 1;
 #pragma unroll
         for (int qx = 0; qx < N; ++qx) {
-          double cvec[3], sdA;
-          fgeom<N, GEOM>(qp, ga, g, ccx, cy, cz, d, s, qx, q, cvec, sdA);
-          flux(cvec, sdA, d, J[qx], Sd[qx], Sa[qx], Sb[qx], rv[qx], rn[qx], ra[qx], rb[qx]);
+          if constexpr (Q3_JOBPRE) {
+            flux(jcv[qx], jsd[qx], d, J[qx], Sd[qx], Sa[qx], Sb[qx], rv[qx], rn[qx], ra[qx], rb[qx]);
+          } else {
+            double cvec[3], sdA;
+            fgeom<N, GEOM>(qp, ga, g, ccx, cy, cz, d, s, qx, q, cvec, sdA);
+            flux(cvec, sdA, d, J[qx], Sd[qx], Sa[qx], Sb[qx], rv[qx], rn[qx], ra[qx], rb[qx]);
+          }
         }
         // transposed x-sweeps: Pv = S^T rv + DS^T ra (tangential a = x), Pb = S^T rb, Pn = S^T rn
         double o[N];

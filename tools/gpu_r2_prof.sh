@@ -1,7 +1,7 @@
 # Fresh ncu --set full captures of the weakest kernels on the current code (round 2, session 3):
 # the odd-n Chebyshev steps (n = 3, 7), the n = 6 Chebyshev step, and k_quad3 on C3.
 set -u
-mkdir -p gpurun_out/pf
+mkdir -p gpurun_out/pf /tmp/pf
 bash tools/ncu_capture.sh pf/cheby_p2 k_kron4 2 1 python tools/prof_driver.py 2 cheby 2
 bash tools/ncu_capture.sh pf/cheby_p6 k_kron4 2 1 python tools/prof_driver.py 6 cheby 2
 bash tools/ncu_capture.sh pf/cheby_p5 k_kron4 2 1 python tools/prof_driver.py 5 cheby 2
