@@ -16,10 +16,12 @@
 //   y: the tile of the row above / below -> M_z on its NL layers (the y-ghost of k_kron4);
 //   x: the c = M_y M_z u field of the adjacent lane by warp shuffle; at the tile edges the
 //      x-neighbour's NL layers are swept by 2*NL*3 helper lanes (z then y), or mirrored.
-// Slot schedule (4 slots, cp.async groups):
-//   u -> S0, z- -> S1, z+ -> S2, y- -> S3;  Z stage;  y+ -> S0 (b -> S1, dinv -> S2);
-//   Y, X stages;  (residual; u -> S3, u_prev -> S0;  P^-1 x, y;  z with dinv;  y, x; update)
-//   result staged in S1 and stored with coalesced addresses.
+// Slot schedule (3 slots S0..S2, cp.async groups; K3_NSLOT=4 is the measured-slower variant):
+//   u -> S0, z- -> S1, z+ -> S2;  Z stage;  y- -> S0, y+ -> S1 (b -> S2);  Y, X stages;
+//   (residual; dinv -> S0, u -> S1, u_prev -> S2;  P^-1 x, y;  z with dinv;  y, x;  update)
+//   result staged in S2 (matvec) or S0 and stored with coalesced addresses.  Three full-cell
+//   slots (20.7 KB per warp) and 168 registers give 10 warps per SM; copying only the NL layers a
+//   neighbour reads (12 warps) measured slower (the per-element 8-byte copies cost more).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -31,7 +33,30 @@
 namespace dgb {
 namespace {
 
-constexpr int N = 3, NN = 9, N3 = 27, TW = 32, NSLOT = 4;
+#ifndef K3_NSLOT
+#define K3_NSLOT 3      // tile slots per warp: 3 (10 warps per SM) or 4 (y- copied with the Z-stage
+                        // tiles, 8 warps per SM; measured slower: p = 2 Chebyshev 103 vs 119 GDoF/s)
+#endif
+#ifndef K3_PF
+#define K3_PF 0         // L2 prefetch at block start: bit 0 the next plane's u tile, bit 1 this tile's
+                        // later Chebyshev streams (b, dinv, u_{j-1}); measured neutral / slower
+#endif
+#ifndef K3_MINB
+#define K3_MINB 10      // __launch_bounds__ min blocks (= warps) per SM: the 3-slot shared-memory limit
+#endif
+
+constexpr int N = 3, NN = 9, N3 = 27, TW = 32, NSLOT = K3_NSLOT;
+// slot roles (see the schedule in the header)
+constexpr int SL_U = 0, SL_ZM = 1, SL_ZP = 2;
+constexpr int SL_YM = NSLOT == 4 ? 3 : 0, SL_YP = NSLOT == 4 ? 0 : 1;
+constexpr int SL_B = NSLOT == 4 ? 1 : 2, SL_D = NSLOT == 4 ? 2 : 0;
+constexpr int SL_UJ = NSLOT == 4 ? 3 : 1, SL_UP = NSLOT == 4 ? 0 : 2;
+constexpr int SL_OUT_APPLY = NSLOT == 4 ? 1 : 2, SL_OUT_CHEBY = NSLOT == 4 ? 1 : 0;
+
+__device__ __forceinline__ void l2pf_range(const double* p, int cnt, int lane) {
+  const char* c = reinterpret_cast<const char*>(p);
+  for (int o = lane * 128; o < cnt * 8; o += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(c + o));
+}
 
 __device__ __forceinline__ int ix(int i, int j, int k) { return k * NN + j * N + i; }
 
@@ -65,7 +90,7 @@ __device__ __forceinline__ void tile_load(double* dst, const double* src, int cn
 }
 
 template <int NL, int MODE>
-__global__ void __launch_bounds__(TW) k_kron3c(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g,
+__global__ void __launch_bounds__(TW, K3_MINB) k_kron3c(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g,
                                                const double* __restrict__ u, double* __restrict__ y,
                                                const __grid_constant__ ChebyArgs ch) {
   __shared__ __align__(16) double S[NSLOT][TW * N3];
@@ -116,11 +141,21 @@ __global__ void __launch_bounds__(TW) k_kron3c(const __grid_constant__ KronParam
     }
   }
 
-  // ---- stage 0: issue the tile copies of the Z and Y stages
-  tile_load(S[0], u + c0 * N3, tcnt, lane);
-  tile_load(S[1], zsrc[0], ncell * zcs[0], lane);
-  tile_load(S[2], zsrc[1], ncell * zcs[1], lane);
-  tile_load(S[3], ym_row >= 0 ? u + (((int64_t)cz * g.Ny + ym_row) * g.Nx + cx0) * N3 : nullptr, tcnt, lane);
+  const double* ym_src = ym_row >= 0 ? u + (((int64_t)cz * g.Ny + ym_row) * g.Nx + cx0) * N3 : nullptr;
+  const double* yp_src = yp_row >= 0 ? u + (((int64_t)cz * g.Ny + yp_row) * g.Nx + cx0) * N3 : nullptr;
+  // ---- stage 0: issue the tile copies of the Z stage (and y- with 4 slots)
+  tile_load(S[SL_U], u + c0 * N3, tcnt, lane);
+  tile_load(S[SL_ZM], zsrc[0], ncell * zcs[0], lane);
+  tile_load(S[SL_ZP], zsrc[1], ncell * zcs[1], lane);
+  if constexpr (NSLOT == 4) tile_load(S[SL_YM], ym_src, tcnt, lane);
+  if constexpr ((K3_PF & 2) != 0 && MODE != KMODE_APPLY) {
+    l2pf_range(ch.b + c0 * N3, tcnt, lane);
+    if (ch.dinv) l2pf_range(ch.dinv + c0 * N3, tcnt, lane);
+    if (!ch.first) l2pf_range(ch.u_prev + c0 * N3, tcnt, lane);
+  }
+  if constexpr ((K3_PF & 1) != 0) {
+    if (cz + 1 < g.zend) l2pf_range(u + (c0 + plane) * N3, tcnt, lane);
+  }
   // edge helpers (lanes < 2*NL*N): z-line (l, j') of the NL i-layers of the x-neighbour
   constexpr int NEDGE = 2 * NL * N;
   const int es = lane / (NL * N), erem = lane - es * (NL * N), el = erem / N, ejk = erem - el * N;
@@ -134,15 +169,16 @@ __global__ void __launch_bounds__(TW) k_kron3c(const __grid_constant__ KronParam
     for (int k = 0; k < N; ++k) eu[k] = __ldg(src + k * NN);
   }
 
-  cpa_wait<1>();   // u, z-, z+ landed (y- may be in flight)
+  if constexpr (NSLOT == 4) cpa_wait<1>();   // u, z-, z+ landed (y- may be in flight)
+  else cpa_wait<0>();
   __syncwarp();
 
   // ---- Z: t = M_z u, a = L_z u + N_z^{+-} u_{z+-}
   double t[N3], a[N3];
   if (active) {
-    const double* us = S[0] + lane * N3;
-    const double* zm_t = S[1] + lane * zcs[0] - zoff[0];
-    const double* zp_t = S[2] + lane * zcs[1] - zoff[1];
+    const double* us = S[SL_U] + lane * N3;
+    const double* zm_t = S[SL_ZM] + lane * zcs[0] - zoff[0];
+    const double* zp_t = S[SL_ZP] + lane * zcs[1] - zoff[1];
 #pragma unroll
     for (int j = 0; j < N; ++j) {
 #pragma unroll
@@ -177,12 +213,17 @@ __global__ void __launch_bounds__(TW) k_kron3c(const __grid_constant__ KronParam
   }
   __syncwarp();   // S0..S2 read, EXT written
 
-  // ---- issue the next copies: y+ (and the Chebyshev b, dinv)
-  tile_load(S[0], yp_row >= 0 ? u + (((int64_t)cz * g.Ny + yp_row) * g.Nx + cx0) * N3 : nullptr, tcnt, lane);
+  // ---- issue the next copies: y+ (y- with 3 slots; the Chebyshev b, and dinv with 4 slots)
+  if constexpr (NSLOT == 3) tile_load(S[SL_YM], ym_src, tcnt, lane);
+  tile_load(S[SL_YP], yp_src, tcnt, lane);
   if constexpr (MODE != KMODE_APPLY) {
-    tile_load(S[1], ch.b + c0 * N3, tcnt, lane);
-    tile_load(S[2], MODE == KMODE_CHEBY_FDM ? nullptr : ch.dinv + c0 * N3, tcnt, lane);
-    cpa_wait<2>();   // y-, y+ landed
+    tile_load(S[SL_B], ch.b + c0 * N3, tcnt, lane);
+    if constexpr (NSLOT == 4) {
+      tile_load(S[SL_D], MODE == KMODE_CHEBY_FDM ? nullptr : ch.dinv + c0 * N3, tcnt, lane);
+      cpa_wait<2>();   // y-, y+ landed
+    } else {
+      cpa_wait<1>();
+    }
   } else {
     cpa_wait<0>();
   }
@@ -198,8 +239,8 @@ __global__ void __launch_bounds__(TW) k_kron3c(const __grid_constant__ KronParam
     for (int j = 0; j < N; ++j) EX[es][el][j][ejk] = o[j];
   }
   if (active) {
-    const double* ym_t = S[3] + lane * N3;
-    const double* yp_t = S[0] + lane * N3;
+    const double* ym_t = S[SL_YM] + lane * N3;
+    const double* yp_t = S[SL_YP] + lane * N3;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       // y-ghosts of this i: (M_z u_{y+-}) at the neighbours' NL layers, [l][k]
@@ -276,7 +317,7 @@ __global__ void __launch_bounds__(TW) k_kron3c(const __grid_constant__ KronParam
   }
 
   if constexpr (MODE == KMODE_APPLY) {
-    double* O = S[1];
+    double* O = S[SL_OUT_APPLY];
     if (active) {
 #pragma unroll
       for (int e = 0; e < N3; ++e) O[lane * N3 + e] = a[e];
@@ -286,22 +327,24 @@ __global__ void __launch_bounds__(TW) k_kron3c(const __grid_constant__ KronParam
     for (int e = lane; e < tcnt; e += 32) yt[e] = O[e];
     return;
   } else {
-    cpa_wait<1>();   // b landed (dinv may be in flight)
+    if constexpr (NSLOT == 4) cpa_wait<1>();   // b landed (dinv may be in flight)
+    else cpa_wait<0>();
     __syncwarp();
     if (active) {   // r = b - A u
-      const double* bs = S[1] + lane * N3;
+      const double* bs = S[SL_B] + lane * N3;
 #pragma unroll
       for (int e = 0; e < N3; ++e) a[e] = bs[e] - a[e];
     }
-    __syncwarp();   // S3 (y-), S0 (y+) and S1 (b) free
-    tile_load(S[3], u + c0 * N3, tcnt, lane);
-    tile_load(S[0], ch.first ? nullptr : ch.u_prev + c0 * N3, tcnt, lane);
+    __syncwarp();   // the y tiles and b are free
+    if constexpr (NSLOT == 3) tile_load(S[SL_D], MODE == KMODE_CHEBY_FDM ? nullptr : ch.dinv + c0 * N3, tcnt, lane);
+    tile_load(S[SL_UJ], u + c0 * N3, tcnt, lane);
+    tile_load(S[SL_UP], ch.first ? nullptr : ch.u_prev + c0 * N3, tcnt, lane);
     double* z = a;   // P^{-1} r in place
     if constexpr (MODE == KMODE_CHEBY_PJ) {
       cpa_wait<2>();   // dinv
       __syncwarp();
       if (active) {
-        const double* ds = S[2] + lane * N3;
+        const double* ds = S[SL_D] + lane * N3;
 #pragma unroll
         for (int e = 0; e < N3; ++e) z[e] *= ds[e];
       }
@@ -336,7 +379,7 @@ __global__ void __launch_bounds__(TW) k_kron3c(const __grid_constant__ KronParam
       cpa_wait<2>();   // dinv
       __syncwarp();
       // z: T^{-T}, diag(A_GL)^{-1}, T^{-1}   (FDM: Z^T, 1/(sum_d c_d lam), Z)
-      const double* ds = S[2] + lane * N3;
+      const double* ds = S[SL_D] + lane * N3;
 #pragma unroll
       for (int j = 0; j < N; ++j) {
 #pragma unroll
@@ -393,10 +436,10 @@ __global__ void __launch_bounds__(TW) k_kron3c(const __grid_constant__ KronParam
     cpa_wait<0>();   // u, u_prev
     __syncwarp();
     // three-term update, Eq. (11): u_{j+1} = u_j + c_prev (u_j - u_{j-1}) + c_z z
-    double* O = S[1];
+    double* O = S[SL_OUT_CHEBY];
     if (active) {
-      const double* uj = S[3] + lane * N3;
-      const double* up = S[0] + lane * N3;
+      const double* uj = S[SL_UJ] + lane * N3;
+      const double* up = S[SL_UP] + lane * N3;
 #pragma unroll
       for (int e = 0; e < N3; ++e) {
         double v = fma(ch.c_z, z[e], uj[e]);

@@ -1,10 +1,8 @@
+# k_kron3c checks on one B200: the p = 2 / C1 / slab parity subset, then an A/B of the given variants at p = 2
 set -u
 mkdir -p gpurun_out/k3c
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_smoother_parity.py tests/test_gpu_halo_loopback.py tests/test_gpu_slab_transport.py -x -q -m gpu -k "p2 or -2- or p-2 or [2- or 2] or C1 or halo or slab or transport or single_cell" > gpurun_out/k3c/tests.log 2>&1; echo "tests rc=$?"
-for v in 0 1; do DG_K3C=$v python bench.py --steps 5 --warmup 3 --quick --degrees 2 2>/dev/null | python -c "
-import sys,json
-for l in sys.stdin:
-  if l.startswith('{'):
-    d=json.loads(l); print('K3C=$v', {p:(round(o['matvec_dofs_per_s']/1e9,1), round(o['cheby_step_dofs_per_s']/1e9,1), round(o['cheby_frac_hbm'],3), round(o.get('cheby_fdm_step_dofs_per_s',0)/1e9,1)) for p,o in d['ops'].items()}, d['clocks']['sm_mhz'])
-" >> gpurun_out/k3c/ab.log; done
-cat gpurun_out/k3c/ab.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_smoother_parity.py tests/test_gpu_halo_loopback.py tests/test_gpu_slab_transport.py tests/test_gpu_user_penalty.py -x -q -m gpu -k "p2 or -2- or p-2 or [2- or 2] or C1 or halo or slab or transport or single_cell" > gpurun_out/k3c/tests.log 2>&1; echo "tests rc=$?"
+tail -3 gpurun_out/k3c/tests.log
+rm -f gpurun_out/ab.log
+bash tools/gpu_r2_ab.sh "${1:-base}" 2
+cat gpurun_out/ab.log
