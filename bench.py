@@ -256,6 +256,12 @@ def geometry_bytes_per_dof(spec):
 
 
 def measured_traffic(workload, kernel, degrees, alg_bytes_per_step):
+    """kernel: one name, or a dict degree -> name (the per-degree kernel of a kernel family)."""
+    names = kernel if isinstance(kernel, dict) else {q: kernel for q in degrees}
+    return _measured_traffic(workload, names, degrees)
+
+
+def _measured_traffic(workload, names, degrees):
     """DRAM bytes (read + write) per launch of the dominant kernel, from the committed
     ncu capture profiles/r1_traffic.json (one `ncu --metrics dram__bytes_read.sum,
     dram__bytes_write.sum` pass of this workload, per degree), averaged over the degrees
@@ -267,19 +273,22 @@ def measured_traffic(workload, kernel, degrees, alg_bytes_per_step):
         return None, "no committed ncu traffic capture"
     with open(p) as f:
         d = json.load(f)
-    ent = d.get(workload, {}).get(kernel)
-    if not ent or any(str(q) not in ent["per_launch_bytes"] for q in degrees):
-        return None, "ncu traffic capture does not cover this configuration"
-    per = [ent["per_launch_bytes"][str(q)] for q in degrees]
-    alg = [ent["algorithmic_bytes"][str(q)] for q in degrees]
-    return float(np.mean(per)), (f"ncu dram read+write per launch, mean over degrees ({ent['source']}); "
+    per, alg, srcs = [], [], set()
+    for q in degrees:
+        ent = d.get(workload, {}).get(names[q])
+        if not ent or str(q) not in ent["per_launch_bytes"]:
+            return None, "ncu traffic capture does not cover this configuration"
+        per.append(ent["per_launch_bytes"][str(q)])
+        alg.append(ent["algorithmic_bytes"][str(q)])
+        srcs.add(ent["source"])
+    return float(np.mean(per)), (f"ncu dram read+write per launch, mean over degrees ({', '.join(sorted(srcs))}); "
                                  f"measured/algorithmic = {sum(per) / sum(alg):.3f}")
 
 
 WORKLOAD_TEXT = {
     "c4": "C4 degree sweep p=2..8, N_p=round(480/(p+1)) cells per direction, matvec + H->GL basis change "
           "+ degree-5 Chebyshev (GL-Jacobi) per degree; Cartesian meshes run the Kronecker form of the same "
-          "operator (Eq. (14); k_kron6 for the p=2 matvec, k_kron4 otherwise), the paper's quadrature "
+          "operator (Eq. (14); the cell-per-thread kernel k_kron3c at p=2, k_kron4 otherwise), the paper's quadrature "
           "formulation is measured separately as c4_paper_formulation",
     "c2": "C2 p=4 32^3 Cartesian, Hermite-like vs nodal Gauss-Lobatto (full-neighbour reads)",
     "c3": "C3 p=5 48^3 curved (amp 0.05), per-quadrature-point geometry, general quadrature kernel",
@@ -457,8 +466,9 @@ def run_ours(a, rank, world, local_rank):
     dom_name = max(dom, key=lambda k: dom[k][1])
     dom = {k: v if v[1] > 0 else [0.0, 1e-30] for k, v in dom.items()}
     ach = dom[dom_name][0] / (dom[dom_name][1] * 1e-3) / 1e9 / world   # per-GPU GB/s
-    if all(sp.geometry == "constant" and sp.deform_amp == 0 for sp in specs):
-        kname = "k_kron4"   # (the p=2 matvec runs k_kron6; the dominant Chebyshev step is k_kron4)
+    cart = all(sp.geometry == "constant" and sp.deform_amp == 0 for sp in specs)
+    if cart:
+        kname = "k_kron4"   # p = 3..8; p = 2 runs the cell-per-thread kernel k_kron3c
     elif all(sp.geometry in ("constant", "per_qpoint") for sp in specs) and os.environ.get("DG_QUAD") != "1":
         kname = "k_quad3"
     else:
@@ -466,7 +476,11 @@ def run_ours(a, rank, world, local_rank):
     bname = "k_bchg4" if os.environ.get("DG_BCHG") == "4" else "k_bchg"   # k_bchg4 default only at p=2, 8
     kernel = {"matvec": f"{kname}<APPLY>", "basis_change": bname,
               "chebyshev_step": f"{kname}<CHEBY_GL>"}[dom_name]
-    traffic, traffic_note = measured_traffic(a.workload, kernel, degrees, dom[dom_name][0] / max(1, a.steps))
+    kper = {q: kernel for q in degrees}
+    if cart and dom_name != "basis_change" and 2 in degrees and os.environ.get("DG_K3C", "1") != "0":
+        kper[2] = kernel.replace("k_kron4", "k_kron3c")
+        kernel = kernel + " (p=3..8) + " + kper[2] + " (p=2)"
+    traffic, traffic_note = measured_traffic(a.workload, kper, degrees, dom[dom_name][0] / max(1, a.steps))
     roofline = {"bound": "hbm", "kernel": kernel,
                 "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                 "traffic": traffic, "traffic_note": traffic_note, "peak_source": hbm_src,

@@ -56,6 +56,16 @@ struct Lay3 {
                         //    shared memory with cp.async at block start (CPBS cells per block)
 #endif
 
+// Chebyshev L1 prefetch of the block's later stream tiles, issued stages ahead (per n):
+// bit 0 b (at the Y stage), bit 1 dinv (at the first P^-1 stage), bit 2 u and u_{j-1} (at the
+// second P^-1 stage).  Measured (tools/gpu_r2_ab.sh, C4): dinv +1.5 % at n = 6, u/u_{j-1} +1-2 %
+// at n = 8, every bit slower at n = 4, 5, 7, 9; K4_L1PF forces one mask for all n.
+#ifdef K4_L1PF
+template <int N> constexpr int k4_l1pf() { return K4_L1PF; }
+#else
+template <int N> constexpr int k4_l1pf() { return N == 6 ? 2 : (N == 8 ? 4 : 0); }
+#endif
+
 #ifndef K4_PREB_ODD
 #define K4_PREB_ODD 1   // odd-n Chebyshev b preload: 0 none, 1 after the Y->X barrier, 2 before it
 #endif
@@ -145,6 +155,15 @@ __device__ __forceinline__ void l2_prefetch(const T* p, int64_t count, int btid,
   const int64_t bytes = count * (int64_t)sizeof(T);
   for (int64_t o = (int64_t)btid * 128; o < bytes; o += (int64_t)bt * 128)
     asm volatile("prefetch.global.L2 [%0];" ::"l"(c + o));
+}
+
+// L1 prefetch of a contiguous range (one prefetch per 128-byte line, block-cooperative)
+template <typename T>
+__device__ __forceinline__ void l1_prefetch(const T* p, int64_t count, int btid, int bt) {
+  const char* c = reinterpret_cast<const char*>(p);
+  const int64_t bytes = count * (int64_t)sizeof(T);
+  for (int64_t o = (int64_t)btid * 128; o < bytes; o += (int64_t)bt * 128)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(c + o));
 }
 
 // M (even-odd) applied to N values read with a stride, written with a stride
@@ -453,6 +472,8 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
   __syncthreads();
 
   // ================================================================ Y
+  const int64_t tile0 = (rowcell + cx0) * N3, tilecnt = (int64_t)ncell * N3;
+  if constexpr ((k4_l1pf<N>() & 1) && MODE != KMODE_APPLY && !kStage) l1_prefetch(ch.b + tile0, tilecnt, btid, BT);
   {
     Real bl[R][N], cl[R][N];
     if (kRL && active) {
@@ -716,6 +737,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
     if constexpr ((MODE == KMODE_CHEBY_GL || MODE == KMODE_CHEBY_FDM) && N % 2 == 0) {
       // even n: x: T^{-T}; y: T^{-T}; z: T^{-T}, diag (coalesced z-lines), T^{-1}; y: T^{-1};
       // x: T^{-1} + update along the x-lines with 128-bit accesses
+      if constexpr ((k4_l1pf<N>() & 2) && MODE == KMODE_CHEBY_GL && !kStage) l1_prefetch(ch.dinv + tile0, tilecnt, btid, BT);
       if (active) {   // x: T^{-T} -> R2 (x-write / y-read)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -742,6 +764,10 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
             for (int k = 0; k < N; ++k) dpre[r][k] = ldsrc<kStage>(dv + k * NN);
           }
         }
+      }
+      if constexpr ((k4_l1pf<N>() & 4) && !kStage) {
+        l1_prefetch(u + tile0, tilecnt, btid, BT);
+        if (!ch.first) l1_prefetch(ch.u_prev + tile0, tilecnt, btid, BT);
       }
       if (active) {   // y: T^{-T} -> R1 (y-write / z-read)
 #pragma unroll
@@ -847,6 +873,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       Real* Z1 = R1 + cslot * LZY.CS;
       Real* Y2 = R2 + cslot * LYX.CS;
       Real* X1 = R1 + cslot * LXZ.CS;
+      if constexpr ((k4_l1pf<N>() & 2) && MODE == KMODE_CHEBY_GL && !kStage) l1_prefetch(ch.dinv + tile0, tilecnt, btid, BT);
       if (active) {   // x: T^{-T}
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -872,6 +899,10 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
             for (int j = 0; j < N; ++j) dpre[r][j] = ldsrc<kStage>(dv + j * N);
           }
         }
+      }
+      if constexpr ((k4_l1pf<N>() & 4) && !kStage) {
+        l1_prefetch(u + tile0, tilecnt, btid, BT);
+        if (!ch.first) l1_prefetch(ch.u_prev + tile0, tilecnt, btid, BT);
       }
       if (active) {   // z: T^{-T}
 #pragma unroll

@@ -30,7 +30,11 @@ per = {}
 for r in rows:
     m = re.search(r"k_kron4<(?:\(int\))?(\d), (?:\(int\))?(\d), (?:\(int\))?(\d)", r[ki])
     m6 = re.search(r"k_kron6<(?:\(int\))?(\d), (?:\(int\))?(\d)", r[ki])
-    if m:
+    m3 = re.search(r"k_kron3c<(?:\(int\))?(\d), (?:\(int\))?(\d)", r[ki])
+    if m3:
+        nl, mode = map(int, m3.groups())
+        n, kern = 3, "k_kron3c"
+    elif m:
         n, nl, mode = map(int, m.groups())
         kern = "k_kron4"
     elif m6:
