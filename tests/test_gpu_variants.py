@@ -1,8 +1,10 @@
 """The opt-in kernel variants (selected by environment variables the library reads once per
 process) against the oracle, each in its own subprocess (tests/_variant_check.py): the
 k_quad general kernel, the n = 5/6/8 alternates of k_kron4, the other output path of
-k_kron4, the z-first basis change at every degree, the L2-prefetch settings and the
-i-plane kernel k_kron6 on and off.  The defaults are covered by test_gpu_parity.py."""
+k_kron4, the z-first basis change at every degree, the L2-prefetch settings, the i-plane
+kernel k_kron6 on and off, and the n = 3 cell-per-thread kernel k_kron3c off (DG_K3C=0, so
+that the n = 3 variants of k_kron4 / k_kron6 are the ones checked).  The defaults are covered
+by test_gpu_parity.py."""
 import os
 import subprocess
 import sys
@@ -17,18 +19,19 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 VARIANTS = [
     ({"DG_QUAD": "1"}, "3", True),
     ({"DG_K4_ALT": "44"}, "4,5,7", False),   # alternates at n = 5, 6, 8 (bits n-3)
-    ({"DG_K4_ALT": "1"}, "2", False),        # n = 3 alternate (padded threads)
+    ({"DG_K4_ALT": "1", "DG_K3C": "0"}, "2", False),   # n = 3 alternate of k_kron4 (padded threads)
     ({"DG_K4_ALT5": "0"}, "4", False),       # n = 5: round 1's unpadded configuration
     ({"DG_K4_ALT7": "0"}, "6", False),       # n = 7: round 1's unpadded configuration
     ({"DG_K4_OUT": "0"}, "3,5", False),
-    ({"DG_K4_OUT": "1"}, "2,4", False),
+    ({"DG_K4_OUT": "1", "DG_K3C": "0"}, "2,4", False),
     ({"DG_BCHG": "4"}, "1,3,4,5,6,7", False),
     ({"DG_BCHG": "1"}, "2,8", False),
     ({"DG_L2PF": "0"}, "5", False),
     ({"DG_L2PF": "2"}, "4", False),
     ({"DG_L2PF": "3"}, "3,6", False),
-    ({"DG_K6": "255"}, "2,3,4,5", False),     # k_kron6 i-plane matvec + Chebyshev for n = 3..6
-    ({"DG_K6": "0"}, "2,3,4,5", False),       # k_kron4 for every n
+    ({"DG_K6": "255", "DG_K3C": "0"}, "2,3,4,5", False),   # k_kron6 i-plane matvec + Chebyshev for n = 3..6
+    ({"DG_K6": "0", "DG_K3C": "0"}, "2,3,4,5", False),     # k_kron4 for every n
+    ({"DG_L2PF": "0", "DG_K3C": "1"}, "2", False),          # k_kron3c (the n = 3 default) without L2 prefetch
 ]
 
 
