@@ -78,7 +78,15 @@ __device__ __forceinline__ void cpa_wait() {
 // are 16-byte aligned; the slot bases are), then one commit (an empty group if src == nullptr)
 __device__ __forceinline__ void tile_load(double* dst, const double* src, int cnt, int lane) {
   if (src) {
-    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const bool al16 = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    if (cnt == TW * N3 && al16) {   // full tile: 432 16-byte copies, unrolled
+#pragma unroll
+      for (int it = 0; it < (TW * N3 / 2) / 32; ++it) cpa16(dst + 2 * (lane + 32 * it), src + 2 * (lane + 32 * it));
+      if constexpr ((TW * N3 / 2) % 32 != 0) {
+        constexpr int e0 = ((TW * N3 / 2) / 32) * 32;
+        if (lane < (TW * N3 / 2) % 32) cpa16(dst + 2 * (e0 + lane), src + 2 * (e0 + lane));
+      }
+    } else if (al16) {
       const int c2 = cnt >> 1;
       for (int e = lane; e < c2; e += 32) cpa16(dst + 2 * e, src + 2 * e);
       if ((cnt & 1) && lane == 0) cpa8(dst + cnt - 1, src + cnt - 1);
@@ -87,6 +95,23 @@ __device__ __forceinline__ void tile_load(double* dst, const double* src, int cn
     }
   }
   cpa_commit();
+}
+
+// coalesced store of a staged tile (full tiles: unrolled 16-byte stores when aligned)
+__device__ __forceinline__ void tile_store(double* dst, const double* src, int cnt, int lane) {
+  if (cnt == TW * N3 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+    for (int it = 0; it < (TW * N3 / 2) / 32; ++it) {
+      const int e = 2 * (lane + 32 * it);
+      *reinterpret_cast<double2*>(dst + e) = *reinterpret_cast<const double2*>(src + e);
+    }
+    if constexpr ((TW * N3 / 2) % 32 != 0) {
+      const int e = 2 * (((TW * N3 / 2) / 32) * 32 + lane);
+      if (lane < (TW * N3 / 2) % 32) *reinterpret_cast<double2*>(dst + e) = *reinterpret_cast<const double2*>(src + e);
+    }
+  } else {
+    for (int e = lane; e < cnt; e += 32) dst[e] = src[e];
+  }
 }
 
 template <int NL, int MODE>
@@ -324,7 +349,7 @@ __global__ void __launch_bounds__(TW, K3_MINB) k_kron3c(const __grid_constant__ 
     }
     __syncwarp();
     double* yt = y + c0 * N3;
-    for (int e = lane; e < tcnt; e += 32) yt[e] = O[e];
+    tile_store(yt, O, tcnt, lane);
     return;
   } else {
     if constexpr (NSLOT == 4) cpa_wait<1>();   // b landed (dinv may be in flight)
@@ -449,7 +474,7 @@ __global__ void __launch_bounds__(TW, K3_MINB) k_kron3c(const __grid_constant__ 
     }
     __syncwarp();
     double* ot = ch.u_next + c0 * N3;
-    for (int e = lane; e < tcnt; e += 32) ot[e] = O[e];
+    tile_store(ot, O, tcnt, lane);
   }
 }
 
