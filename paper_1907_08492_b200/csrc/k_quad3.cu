@@ -85,8 +85,17 @@ struct Q3Layout {
 __device__ __forceinline__ int at(const Lay3& L, int i, int j, int k) { return i + j * L.Pj + k * L.Pk; }
 
 // register cap so that the smem-limited number of resident blocks (at most 2) fits
+#ifndef Q3_MAXREG
+#define Q3_MAXREG 0     // > 0: register cap override (e.g. 255: one block per SM, room for early loads)
+#endif
+template <int N, int NL>
+constexpr int q3_maxreg_auto();
 template <int N, int NL>
 constexpr int q3_maxreg() {
+  return Q3_MAXREG > 0 ? Q3_MAXREG : q3_maxreg_auto<N, NL>();
+}
+template <int N, int NL>
+constexpr int q3_maxreg_auto() {
   constexpr int b0 = (227 * 1024) / Q3Layout<N, NL>::bytes();
   constexpr int b = b0 < 1 ? 1 : (b0 > 2 ? 2 : b0);
   constexpr int warps = (Q3Layout<N, NL>::CPB * N * N + 31) / 32;
