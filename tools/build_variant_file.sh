@@ -6,7 +6,7 @@ cd /root/repo
 python -m paper_1907_08492_b200.build > /dev/null
 mkdir -p variants /tmp/variant_$name
 src=paper_1907_08492_b200/csrc/$file
-tmp=paper_1907_08492_b200/csrc/variant_tmp_${name}.cu
+tmp=/tmp/variant_$name/variant_tmp_${name}.cu   # outside csrc/ so that concurrent main builds never see it
 sed "$expr" $src > $tmp
 cmp -s $src $tmp && { echo "sed changed nothing"; rm $tmp; exit 1; }
 inc=$(python -c "import sys; sys.path.insert(0,'paper_1907_08492_b200'); import build; print(build._nccl_dirs()[0])")
