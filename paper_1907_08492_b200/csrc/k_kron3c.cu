@@ -41,6 +41,9 @@ namespace {
 #define K3_PF 0         // L2 prefetch at block start: bit 0 the next plane's u tile, bit 1 this tile's
                         // later Chebyshev streams (b, dinv, u_{j-1}); measured neutral / slower
 #endif
+#ifndef K3_FAST
+#define K3_FAST 1       // full-tile specialisation where the launch allows it (0: always the general kernel)
+#endif
 #ifndef K3_MINB
 #define K3_MINB 10      // __launch_bounds__ min blocks (= warps) per SM: the 3-slot shared-memory limit
 #endif
@@ -76,16 +79,18 @@ __device__ __forceinline__ void cpa_wait() {
 
 // warp-cooperative copy of cnt contiguous doubles into a slot (16-byte copies when both ends
 // are 16-byte aligned; the slot bases are), then one commit (an empty group if src == nullptr)
+template <bool FAST>
 __device__ __forceinline__ void tile_load(double* dst, const double* src, int cnt, int lane) {
   if (src) {
-    const bool al16 = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-    if (cnt == TW * N3 && al16) {   // full tile: 432 16-byte copies, unrolled
+    const bool al16 = FAST || (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    if (FAST || (cnt == TW * N3 && al16)) {   // full tile: 432 16-byte copies, unrolled
 #pragma unroll
       for (int it = 0; it < (TW * N3 / 2) / 32; ++it) cpa16(dst + 2 * (lane + 32 * it), src + 2 * (lane + 32 * it));
       if constexpr ((TW * N3 / 2) % 32 != 0) {
         constexpr int e0 = ((TW * N3 / 2) / 32) * 32;
         if (lane < (TW * N3 / 2) % 32) cpa16(dst + 2 * (e0 + lane), src + 2 * (e0 + lane));
       }
+    } else if constexpr (FAST) {
     } else if (al16) {
       const int c2 = cnt >> 1;
       for (int e = lane; e < c2; e += 32) cpa16(dst + 2 * e, src + 2 * e);
@@ -98,8 +103,9 @@ __device__ __forceinline__ void tile_load(double* dst, const double* src, int cn
 }
 
 // coalesced store of a staged tile (full tiles: unrolled 16-byte stores when aligned)
+template <bool FAST>
 __device__ __forceinline__ void tile_store(double* dst, const double* src, int cnt, int lane) {
-  if (cnt == TW * N3 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+  if (FAST || (cnt == TW * N3 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
     for (int it = 0; it < (TW * N3 / 2) / 32; ++it) {
       const int e = 2 * (lane + 32 * it);
@@ -109,12 +115,16 @@ __device__ __forceinline__ void tile_store(double* dst, const double* src, int c
       const int e = 2 * (((TW * N3 / 2) / 32) * 32 + lane);
       if (lane < (TW * N3 / 2) % 32) *reinterpret_cast<double2*>(dst + e) = *reinterpret_cast<const double2*>(src + e);
     }
-  } else {
+  } else if constexpr (!FAST) {
     for (int e = lane; e < cnt; e += 32) dst[e] = src[e];
   }
 }
 
-template <int NL, int MODE>
+// FAST: every tile of the launch is a full 32-cell tile with 16-byte aligned sources and
+// destinations and no slab halo (the launcher checks), so the copy/store fallbacks, the
+// partial-tile guards and the halo path are compiled out (smaller code: fewer instruction
+// fetch stalls)
+template <int NL, int MODE, bool FAST>
 __global__ void __launch_bounds__(TW, K3_MINB) k_kron3c(const __grid_constant__ KronParams kp, const __grid_constant__ GridArgs g,
                                                const double* __restrict__ u, double* __restrict__ y,
                                                const __grid_constant__ ChebyArgs ch) {
@@ -125,7 +135,7 @@ __global__ void __launch_bounds__(TW, K3_MINB) k_kron3c(const __grid_constant__ 
   const int lane = threadIdx.x;
   const int cx0 = blockIdx.x * TW, cy = blockIdx.y, cz = g.zbeg + blockIdx.z;
   const int ncell = g.Nx - cx0 < TW ? g.Nx - cx0 : TW;
-  const bool active = lane < ncell;
+  const bool active = FAST || lane < ncell;
   const int64_t plane = (int64_t)g.Nx * g.Ny;
   const int64_t rowcell = ((int64_t)cz * g.Ny + cy) * g.Nx;
   const int64_t c0 = rowcell + cx0;   // first cell of the tile
@@ -158,7 +168,7 @@ __global__ void __launch_bounds__(TW, K3_MINB) k_kron3c(const __grid_constant__ 
         zmir[s] = true;
       } else if (src == ZSRC_LOCAL) {   // periodic wrap inside the slab
         zsrc[s] = u + (c0 + (s ? -(int64_t)(g.nz - 1) : (int64_t)(g.nz - 1)) * plane) * N3;
-      } else {                          // slab halo: [cell][NL][n][n]
+      } else if constexpr (!FAST) {     // slab halo: [cell][NL][n][n]
         zsrc[s] = (s ? g.halo_hi : g.halo_lo) + ((int64_t)cy * g.Nx + cx0) * (NL * NN);
         zcs[s] = NL * NN;
         zoff[s] = s ? 0 : (N - NL) * NN;
@@ -169,10 +179,10 @@ __global__ void __launch_bounds__(TW, K3_MINB) k_kron3c(const __grid_constant__ 
   const double* ym_src = ym_row >= 0 ? u + (((int64_t)cz * g.Ny + ym_row) * g.Nx + cx0) * N3 : nullptr;
   const double* yp_src = yp_row >= 0 ? u + (((int64_t)cz * g.Ny + yp_row) * g.Nx + cx0) * N3 : nullptr;
   // ---- stage 0: issue the tile copies of the Z stage (and y- with 4 slots)
-  tile_load(S[SL_U], u + c0 * N3, tcnt, lane);
-  tile_load(S[SL_ZM], zsrc[0], ncell * zcs[0], lane);
-  tile_load(S[SL_ZP], zsrc[1], ncell * zcs[1], lane);
-  if constexpr (NSLOT == 4) tile_load(S[SL_YM], ym_src, tcnt, lane);
+  tile_load<FAST>(S[SL_U], u + c0 * N3, tcnt, lane);
+  tile_load<FAST>(S[SL_ZM], zsrc[0], ncell * zcs[0], lane);
+  tile_load<FAST>(S[SL_ZP], zsrc[1], ncell * zcs[1], lane);
+  if constexpr (NSLOT == 4) tile_load<FAST>(S[SL_YM], ym_src, tcnt, lane);
   if constexpr ((K3_PF & 2) != 0 && MODE != KMODE_APPLY) {
     l2pf_range(ch.b + c0 * N3, tcnt, lane);
     if (ch.dinv) l2pf_range(ch.dinv + c0 * N3, tcnt, lane);
@@ -239,12 +249,12 @@ __global__ void __launch_bounds__(TW, K3_MINB) k_kron3c(const __grid_constant__ 
   __syncwarp();   // S0..S2 read, EXT written
 
   // ---- issue the next copies: y+ (y- with 3 slots; the Chebyshev b, and dinv with 4 slots)
-  if constexpr (NSLOT == 3) tile_load(S[SL_YM], ym_src, tcnt, lane);
-  tile_load(S[SL_YP], yp_src, tcnt, lane);
+  if constexpr (NSLOT == 3) tile_load<FAST>(S[SL_YM], ym_src, tcnt, lane);
+  tile_load<FAST>(S[SL_YP], yp_src, tcnt, lane);
   if constexpr (MODE != KMODE_APPLY) {
-    tile_load(S[SL_B], ch.b + c0 * N3, tcnt, lane);
+    tile_load<FAST>(S[SL_B], ch.b + c0 * N3, tcnt, lane);
     if constexpr (NSLOT == 4) {
-      tile_load(S[SL_D], MODE == KMODE_CHEBY_FDM ? nullptr : ch.dinv + c0 * N3, tcnt, lane);
+      tile_load<FAST>(S[SL_D], MODE == KMODE_CHEBY_FDM ? nullptr : ch.dinv + c0 * N3, tcnt, lane);
       cpa_wait<2>();   // y-, y+ landed
     } else {
       cpa_wait<1>();
@@ -349,7 +359,7 @@ __global__ void __launch_bounds__(TW, K3_MINB) k_kron3c(const __grid_constant__ 
     }
     __syncwarp();
     double* yt = y + c0 * N3;
-    tile_store(yt, O, tcnt, lane);
+    tile_store<FAST>(yt, O, tcnt, lane);
     return;
   } else {
     if constexpr (NSLOT == 4) cpa_wait<1>();   // b landed (dinv may be in flight)
@@ -361,9 +371,9 @@ __global__ void __launch_bounds__(TW, K3_MINB) k_kron3c(const __grid_constant__ 
       for (int e = 0; e < N3; ++e) a[e] = bs[e] - a[e];
     }
     __syncwarp();   // the y tiles and b are free
-    if constexpr (NSLOT == 3) tile_load(S[SL_D], MODE == KMODE_CHEBY_FDM ? nullptr : ch.dinv + c0 * N3, tcnt, lane);
-    tile_load(S[SL_UJ], u + c0 * N3, tcnt, lane);
-    tile_load(S[SL_UP], ch.first ? nullptr : ch.u_prev + c0 * N3, tcnt, lane);
+    if constexpr (NSLOT == 3) tile_load<FAST>(S[SL_D], MODE == KMODE_CHEBY_FDM ? nullptr : ch.dinv + c0 * N3, tcnt, lane);
+    tile_load<FAST>(S[SL_UJ], u + c0 * N3, tcnt, lane);
+    tile_load<FAST>(S[SL_UP], ch.first ? nullptr : ch.u_prev + c0 * N3, tcnt, lane);
     double* z = a;   // P^{-1} r in place
     if constexpr (MODE == KMODE_CHEBY_PJ) {
       cpa_wait<2>();   // dinv
@@ -474,9 +484,11 @@ __global__ void __launch_bounds__(TW, K3_MINB) k_kron3c(const __grid_constant__ 
     }
     __syncwarp();
     double* ot = ch.u_next + c0 * N3;
-    tile_store(ot, O, tcnt, lane);
+    tile_store<FAST>(ot, O, tcnt, lane);
   }
 }
+
+inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <int NL, int MODE>
 cudaError_t launch_t(const KronParams& kp, const GridArgs& g, const double* u, double* y, const ChebyArgs& ch,
@@ -485,7 +497,14 @@ cudaError_t launch_t(const KronParams& kp, const GridArgs& g, const double* u, d
   if (planes <= 0 || g.Nx <= 0 || g.Ny <= 0) return cudaSuccess;
   if (g.Ny > 65535 || planes > 65535) return cudaErrorInvalidValue;
   const dim3 grid((g.Nx + TW - 1) / TW, g.Ny, planes);
-  k_kron3c<NL, MODE><<<grid, TW, 0, s>>>(kp, g, u, y, ch);
+  const bool ptrs = MODE == KMODE_APPLY ? al16(u) && al16(y)
+                                        : al16(u) && al16(ch.b) && al16(ch.u_next) && (ch.first || al16(ch.u_prev)) &&
+                                              (MODE == KMODE_CHEBY_FDM || al16(ch.dinv));
+  const bool fast = K3_FAST && g.Nx % TW == 0 && g.zlo != ZSRC_HALO && g.zhi != ZSRC_HALO && ptrs;
+  if (fast)
+    k_kron3c<NL, MODE, true><<<grid, TW, 0, s>>>(kp, g, u, y, ch);
+  else
+    k_kron3c<NL, MODE, false><<<grid, TW, 0, s>>>(kp, g, u, y, ch);
   return cudaGetLastError();
 }
 

@@ -473,3 +473,34 @@ def test_apply_host_buffers(spec):
         torch.cuda.synchronize()
         assert np.array_equal(yh.numpy(), yd), pinned
     assert _rel(yd, _oracle(spec).apply(u)) <= TOL
+
+
+@pytest.mark.parametrize("nc,bc", [((32, 2, 3), ("periodic", "dirichlet", "dirichlet")),
+                                   ((64, 2, 2), ("dirichlet", "periodic", "periodic"))])
+@pytest.mark.parametrize("basis", ["hermite", "gl"])
+def test_k3c_full_tiles(nc, bc, basis):
+    """k_kron3c's full-tile specialisation (rows a multiple of 32 cells, aligned vectors, no
+    slab halo: the launcher picks the FAST kernel) for the matvec and the fused Chebyshev step
+    with every inner preconditioner, against the oracle."""
+    _needs_gpu()
+    from oracle import fdm
+    from oracle import smoother as sm
+    from oracle.geometry import mesh_from_spec
+    from oracle.sipg import SIPG
+    p = 2
+    spec = MeshSpec(degree=p, n_cells=nc, bc=bc, basis=basis, seed=170)
+    u = uniform_vector(spec.n_dofs, spec.seed)
+    om = mesh_from_spec(spec)
+    H = SIPG(om, p, basis)
+    m = _gpu_mesh(spec)
+    assert _rel(m.apply_laplace(_dev(u)).cpu().numpy(), H.apply(u)) <= TOL
+    if basis != "hermite":
+        return
+    b = uniform_vector(spec.n_dofs, 171)
+    h = tuple(1.0 / c for c in nc)
+    for inner, Pc in (("gl_jacobi", sm.GLJacobi(SIPG(om, p, "gl"))), ("point_jacobi", sm.PointJacobi(H)),
+                      ("fdm", fdm.FDM(p, h))):
+        ref = sm.chebyshev(H.apply, Pc, b, u, 3, 2.4)
+        x = _dev(u)
+        m.chebyshev_smooth(_dev(b), x, 2.4, degree=3, inner=inner)
+        assert _rel(x.cpu().numpy(), ref) <= TOL, inner
