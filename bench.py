@@ -266,17 +266,19 @@ def _measured_traffic(workload, names, degrees):
     ncu capture profiles/r1_traffic.json (one `ncu --metrics dram__bytes_read.sum,
     dram__bytes_write.sum` pass of this workload, per degree), averaged over the degrees
     like `achieved`; None if the capture does not cover this workload/kernel."""
-    p = os.path.join(ROOT, "profiles", "r2_traffic.json")
-    if not os.path.exists(p):
-        p = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    if not os.path.exists(p):
+    caps = []
+    for fn in ("r2s4_traffic.json", "r2_traffic.json", "r1_traffic.json"):   # newest capture first
+        p = os.path.join(ROOT, "profiles", fn)
+        if os.path.exists(p):
+            with open(p) as f:
+                caps.append(json.load(f))
+    if not caps:
         return None, "no committed ncu traffic capture"
-    with open(p) as f:
-        d = json.load(f)
     per, alg, srcs = [], [], set()
     for q in degrees:
-        ent = d.get(workload, {}).get(names[q])
-        if not ent or str(q) not in ent["per_launch_bytes"]:
+        ent = next((e for e in (d.get(workload, {}).get(names[q]) for d in caps)
+                    if e and str(q) in e["per_launch_bytes"]), None)
+        if ent is None:
             return None, "ncu traffic capture does not cover this configuration"
         per.append(ent["per_launch_bytes"][str(q)])
         alg.append(ent["algorithmic_bytes"][str(q)])
@@ -288,7 +290,8 @@ def _measured_traffic(workload, names, degrees):
 WORKLOAD_TEXT = {
     "c4": "C4 degree sweep p=2..8, N_p=round(480/(p+1)) cells per direction, matvec + H->GL basis change "
           "+ degree-5 Chebyshev (GL-Jacobi) per degree; Cartesian meshes run the Kronecker form of the same "
-          "operator (Eq. (14); the cell-per-thread kernel k_kron3c at p=2, k_kron4 otherwise), the paper's quadrature "
+          "operator (Eq. (14); the cell-per-thread kernel k_kron3c at p=2, k_kron4 otherwise; the Chebyshev "
+          "steps at p=3,4,6,7,8 on the transformed residual (T^-T)^(x)3 (b - Au)), the paper's quadrature "
           "formulation is measured separately as c4_paper_formulation",
     "c2": "C2 p=4 32^3 Cartesian, Hermite-like vs nodal Gauss-Lobatto (full-neighbour reads)",
     "c3": "C3 p=5 48^3 curved (amp 0.05), per-quadrature-point geometry, general quadrature kernel",
@@ -477,9 +480,22 @@ def run_ours(a, rank, world, local_rank):
     kernel = {"matvec": f"{kname}<APPLY>", "basis_change": bname,
               "chebyshev_step": f"{kname}<CHEBY_GL>"}[dom_name]
     kper = {q: kernel for q in degrees}
-    if cart and dom_name != "basis_change" and 2 in degrees and os.environ.get("DG_K3C", "1") != "0":
-        kper[2] = kernel.replace("k_kron4", "k_kron3c")
-        kernel = kernel + " (p=3..8) + " + kper[2] + " (p=2)"
+    k3c = os.environ.get("DG_K3C", "1") != "0"
+    if cart and dom_name == "chebyshev_step":
+        # transformed-residual step (KMODE_CHEBY_GLT) where bit n-3 of DG_CHEBY_GLT is set (the
+        # library's default mask 0x77: every n but 6), after one k_bchg pass b~ = (T^-T)^(x)3 b per sweep
+        glt = int(os.environ.get("DG_CHEBY_GLT", "119"))
+        for q in degrees:
+            if (glt >> (q - 2)) & 1 and not (q == 2 and k3c):
+                kper[q] = "k_kron4<CHEBY_GLT>"
+        gq = [q for q in degrees if kper[q].endswith("GLT>")]
+        if gq:
+            dq = [q for q in degrees if q not in gq and not (q == 2 and k3c)]
+            kernel = (f"k_kron4<CHEBY_GLT> (p={','.join(map(str, gq))}; + one k_bchg pass per sweep)"
+                      + (f" + k_kron4<CHEBY_GL> (p={','.join(map(str, dq))})" if dq else ""))
+    if cart and dom_name != "basis_change" and 2 in degrees and k3c:
+        kper[2] = f"k_kron3c<{'APPLY' if dom_name == 'matvec' else 'CHEBY_GL'}>"
+        kernel = kernel + (" (p=3..8)" if "(p=" not in kernel else "") + " + " + kper[2] + " (p=2)"
     traffic, traffic_note = measured_traffic(a.workload, kper, degrees, dom[dom_name][0] / max(1, a.steps))
     roofline = {"bound": "hbm", "kernel": kernel,
                 "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
@@ -487,7 +503,8 @@ def run_ours(a, rank, world, local_rank):
                 "per_degree_frac": {k: (o["cheby_frac_hbm"] if dom_name == "chebyshev_step" else o["matvec_frac_hbm"])
                                     for k, o in ops.items()},
                 "note": "achieved = algorithmic bytes (matvec/basis change 16 B/DoF, Chebyshev step "
-                        "40 B/DoF, first step 32) / summed CUDA-event time of that op, per GPU"}
+                        "40 B/DoF, first step 32; the transformed-residual sweep's extra k_bchg pass on b "
+                        "is not counted) / summed CUDA-event time of that op, per GPU"}
     mv_gbs = dom["matvec"][0] / (dom["matvec"][1] * 1e-3) / 1e9 / world
     matvec_roof = {"achieved_gbs": mv_gbs, "frac_hbm": mv_gbs / hbm_peak}
     if fp64_peak:

@@ -164,6 +164,64 @@ bool fdm_setup(const double* L, const double* M, int n, KronParams& kp) {
   return ns == hs && na == ha;
 }
 
+void pack_eo(const double* A, int n, double* out);
+
+// Tables of the transformed-residual Chebyshev step (KronParams::Mt/Lt/Ft, KMODE_CHEBY_GLT):
+// T^{-T} times Mhat, L_d and the neighbour block N^-_d, accumulated in long double.  Returns
+// false (mode unavailable) unless the products keep the reflection symmetry the even-odd
+// packing assumes: A[n-1-i][n-1-j] = A[i][j] and (T^{-T} N^+)[n-1-i][NL-1-l] = (T^{-T} N^-)[i][l].
+bool glt_setup(const Tables1D& t, int n, int NL, const double* h, KronParams& kp) {
+  using R = long double;
+  const double V = h[0] * h[1] * h[2];
+  auto mul = [&](const double* A, int cols, int lda, int c0, double sc, R* out) {   // T^{-T} (sc A[:, c0:c0+cols])
+    for (int i = 0; i < n; ++i)
+      for (int c = 0; c < cols; ++c) {
+        R acc = 0;
+        for (int k = 0; k < n; ++k) acc += (R)t.Tinv[k * n + i] * ((R)sc * (R)A[k * lda + c0 + c]);
+        out[i * cols + c] = acc;
+      }
+  };
+  auto centro = [&](const R* A) {
+    R mx = 0, err = 0;
+    for (int q = 0; q < n * n; ++q) mx = std::max(mx, std::fabs(A[q]));
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) err = std::max(err, std::fabs(A[i * n + j] - A[(n - 1 - i) * n + n - 1 - j]));
+    return err <= 1e-13L * mx;
+  };
+  R A[kMaxN * kMaxN];
+  double Ad[kMaxN * kMaxN];
+  mul(t.Mhat, n, n, 0, 1.0, A);
+  if (!centro(A)) return false;
+  for (int q = 0; q < n * n; ++q) Ad[q] = (double)A[q];
+  pack_eo(Ad, n, kp.Mt);
+  const int H = n / 2;
+  for (int dd = 0; dd < 3; ++dd) {
+    const double sc = V / (h[dd] * h[dd]);
+    mul(t.Lhat, n, n, 0, sc, A);
+    if (!centro(A)) return false;
+    for (int q = 0; q < n * n; ++q) Ad[q] = (double)A[q];
+    pack_eo(Ad, n, kp.Lt[dd]);
+    R Pm[kMaxN * 2], Pp[kMaxN * 2];
+    mul(t.Nm, NL, n, n - NL, sc, Pm);   // own rows x neighbour layers [n-NL, n)
+    mul(t.Np, NL, n, 0, sc, Pp);        // own rows x neighbour layers [0, NL)
+    R mx = 0, err = 0;
+    for (int i = 0; i < n; ++i)
+      for (int l = 0; l < NL; ++l) {
+        mx = std::max(mx, std::fabs(Pm[i * NL + l]));
+        err = std::max(err, std::fabs(Pp[(n - 1 - i) * NL + (NL - 1 - l)] - Pm[i * NL + l]));
+      }
+    if (!(err <= 1e-13L * mx)) return false;
+    int o = 0;
+    for (int i = 0; i < H; ++i)
+      for (int l = 0; l < NL; ++l) kp.Ft[dd][o++] = (double)(0.5L * (Pm[i * NL + l] + Pm[(n - 1 - i) * NL + l]));
+    for (int i = 0; i < H; ++i)
+      for (int l = 0; l < NL; ++l) kp.Ft[dd][o++] = (double)(0.5L * (Pm[i * NL + l] - Pm[(n - 1 - i) * NL + l]));
+    if (n & 1)
+      for (int l = 0; l < NL; ++l) kp.Ft[dd][o++] = (double)Pm[H * NL + l];
+  }
+  return true;
+}
+
 void pack_eo(const double* A, int n, double* out) {
   const int h = n / 2, mid = h;
   int o = 0;
@@ -232,6 +290,8 @@ struct dg_mesh_s {
   int rank = 0, nranks = 1;
   int64_t launches = 0;
   bool fdm_ok = false;            // FDM tables built (Cartesian meshes)
+  bool glt_ok = false;            // transformed-residual Chebyshev tables built (KronParams::Mt/Lt/Ft)
+  double* d_bt = nullptr;         // (T^{-T})^{(x)3} b of the current GLT Chebyshev sweep
   double* d_dot = nullptr;        // dot-product scratch: partials + result
   // fp32 path: rounded Kronecker tables and inverse diagonals
   KronParamsF kpf{};
@@ -281,6 +341,18 @@ bool kron3c_use(int n, int NL) {
     return e ? std::atoi(e) : 1;
   }();
   return v != 0 && kron3c_supported(n, NL);
+}
+
+// transformed-residual GL-Jacobi Chebyshev (KMODE_CHEBY_GLT) where the step runs on k_kron4 and
+// bit n-3 of DG_CHEBY_GLT is set.  Default by measurement (same-box A/B, C4, GDoF/s per step,
+// direct -> transformed): n = 4 91.5 -> 93.3, n = 5 77.3 -> 81.2, n = 6 98.3 -> 95.9 (off),
+// n = 7 70.2 -> 71.4, n = 8 85.8 -> 102.9, n = 9 82.6 -> 87.1; n = 3 runs k_kron3c (direct step)
+bool glt_use(dg_mesh m) {
+  static const int mask = [] {
+    const char* e = std::getenv("DG_CHEBY_GLT");
+    return e ? std::atoi(e) : 0x77;   // all n but 6
+  }();
+  return ((mask >> (m->n - 3)) & 1) && m->glt_ok && m->cartesian && kron_v4(m->n) && !kron3c_use(m->n, m->NL);
 }
 
 // general kernel selection: k_quad3 (z-first) unless DG_QUAD=1 asks for k_quad.cu
@@ -652,6 +724,7 @@ dg_status dg_mesh_setup(const dg_mesh_desc* d, dg_mesh* out) {
     pack_eo(t.Tinv, n, kp.Ti);
     for (int dd = 0; dd < 3; ++dd) kp.cdir[dd] = V / (m->h[dd] * m->h[dd]);
     m->fdm_ok = m->cartesian && fdm_setup(t.Lhat, t.Mhat, n, kp);
+    m->glt_ok = m->cartesian && NL == 2 && glt_setup(t, n, NL, m->h, kp);
   }
 
   // z sources and halo
@@ -813,6 +886,7 @@ dg_status dg_mesh_destroy(dg_mesh m) {
   cudaFree(m->d_jinv);
   for (int d = 0; d < 3; ++d) cudaFree(m->d_usig[d]);
   cudaFree(m->d_dinv_gl);
+  cudaFree(m->d_bt);
   cudaFree(m->d_dinv_pj);
   cudaFree(m->d_dot);
   cudaFree(m->d_dinv_gl_f);
@@ -1042,7 +1116,18 @@ dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* wor
   double** dsrc = fdm ? &dnone : (gl ? &m->d_dinv_gl : &m->d_dinv_pj);
   dg_status st = fdm ? DG_OK : build_diag(m, inner == DG_INNER_GL_JACOBI, dsrc, s);
   if (st != DG_OK) return st;
-  const int mode = fdm ? KMODE_CHEBY_FDM : (gl ? KMODE_CHEBY_GL : KMODE_CHEBY_PJ);
+  int mode = fdm ? KMODE_CHEBY_FDM : (gl ? KMODE_CHEBY_GL : KMODE_CHEBY_PJ);
+  // GL-Jacobi on the k_kron4 path: transform the rhs once, b~ = (T^{-T})^{(x)3} b, and run the
+  // steps on the transformed residual (KMODE_CHEBY_GLT: three P^{-1} sweeps and two
+  // transposes fewer per step).  DG_CHEBY_GLT=0 keeps the direct step.
+  const double* bstep = b;
+  if (mode == KMODE_CHEBY_GL && glt_use(m)) {
+    if (!m->d_bt) CUDA_TRY(cudaMalloc(&m->d_bt, sizeof(double) * (size_t)std::max<int64_t>(nd, 1)));
+    st = dg_basis_change(m, DG_BCHG_GL_TO_H_T, b, m->d_bt, stream);
+    if (st != DG_OK) return st;
+    bstep = m->d_bt;
+    mode = KMODE_CHEBY_GLT;
+  }
 
   // storage of u_j so that u_degree lands in x (in-place updates over u_{j-1})
   double* buf[3] = {x, W0, W1};
@@ -1062,7 +1147,7 @@ dg_status dg_chebyshev_smooth(dg_mesh m, const double* b, double* x, double* wor
   double rho = 1.0 / sigma1;
   for (int j = 0; j < degree; ++j) {
     ChebyArgs ch{};
-    ch.b = b;
+    ch.b = bstep;
     ch.dinv = *dsrc;
     ch.u_next = buf[where[j + 1]];
     if (j == 0) {
@@ -1137,7 +1222,9 @@ dg_status run_pass(dg_mesh m, int mode, bool kron, const double* u, double* y, c
     if (ze <= zb) return DG_OK;
     GridArgs g = grid_args(m, zb, ze);
     cudaError_t e;
-    if (kron && kron3c_use(m->n, m->NL))
+    if (mode == KMODE_CHEBY_GLT)
+      e = launch_kron4(m->n, m->NL, mode, m->kp, g, u, y, ch, s);
+    else if (kron && kron3c_use(m->n, m->NL))
       e = launch_kron3c(m->NL, mode, m->kp, g, u, y, ch, s);
     else if (kron && kron6_use(m->n, m->NL, mode))
       e = launch_kron6(m->n, mode, m->kp, g, u, y, ch, s);

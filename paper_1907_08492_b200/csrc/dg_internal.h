@@ -33,6 +33,17 @@ struct KronParamsT {
   Real Za[kMaxN * kMaxN];
   Real lam[kMaxN];
   Real cdir[3];
+  // Transformed-residual GL-Jacobi Chebyshev step (KMODE_CHEBY_GLT, NL = 2 only): the 1D
+  // factors premultiplied by T^{-T}, so that the three matvec sweeps yield (T^{-T})^{(x)3} A u
+  // directly (Kronecker mixed product); the rhs is transformed once per sweep.
+  //   Mt = T^{-T} Mhat, Lt[d] = T^{-T} L_d (even-odd packed, parity +1)
+  //   Ft[d]: P = T^{-T} N^-_d (n x NL, own rows x neighbour layers [n-NL, n)), even-odd packed
+  //          with the mirror image T^{-T} N^+_d[n-1-i][NL-1-l] = P[i][l]:
+  //          Fe[i][l] = (P[i][l] + P[n-1-i][l]) / 2, Fo[i][l] = (P[i][l] - P[n-1-i][l]) / 2
+  //          (i < n/2), then Fm[l] = P[n/2][l] (odd n)
+  Real Mt[kEO];
+  Real Lt[3][kEO];
+  Real Ft[3][kMaxN * 2];
 };
 using KronParams = KronParamsT<double>;
 using KronParamsF = KronParamsT<float>;   // fp32 path, rounded from KronParams
@@ -50,7 +61,8 @@ struct GridArgs {
   int l2pf;                   // k_kron4/k_quad: L2 prefetch of the next plane's tile (DG_L2PF, default 1)
 };
 
-enum { KMODE_APPLY = 0, KMODE_CHEBY_GL = 1, KMODE_CHEBY_PJ = 2, KMODE_CHEBY_FDM = 3 };
+enum { KMODE_APPLY = 0, KMODE_CHEBY_GL = 1, KMODE_CHEBY_PJ = 2, KMODE_CHEBY_FDM = 3,
+       KMODE_CHEBY_GLT = 4 };   // GLT: GL-Jacobi step on the transformed residual (k_kron4, NL = 2)
 
 template <typename Real>
 struct ChebyArgsT {

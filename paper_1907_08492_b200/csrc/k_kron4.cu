@@ -108,7 +108,7 @@ constexpr int imax(int a, int b) { return a > b ? a : b; }
 template <int N, int NL, int ALT = 0, int MODE = KMODE_APPLY>
 struct K4Layout {
   // the x->z layout is only used by point Jacobi and by the odd-n Chebyshev order
-  static constexpr bool USE_XZ = MODE == KMODE_CHEBY_PJ || (N % 2 == 1 && MODE != KMODE_APPLY);
+  static constexpr bool USE_XZ = MODE == KMODE_CHEBY_PJ || (N % 2 == 1 && MODE != KMODE_APPLY && MODE != KMODE_CHEBY_GLT);
   // K4_STAGE: Chebyshev streams staged in smem (b, u_{j-1}, and dinv unless FDM)
   static constexpr int NSTG = (K4_STAGE && MODE != KMODE_APPLY) ? (MODE == KMODE_CHEBY_FDM ? 2 : 3) : 0;
   static constexpr int R = K4C<N, ALT>::R, CPB = NSTG ? K4C<N, ALT>::CPBS : K4C<N, ALT>::CPB;
@@ -177,6 +177,89 @@ __device__ __forceinline__ void mass_line(const T* __restrict__ M, const T* src,
   for (int k = 0; k < N; ++k) dst[k * ds] = o[k];
 }
 
+// KMODE_CHEBY_GLT: y = A s (+ A2 s2) + T^{-T} (N^- gm + N^+ gp), the neighbour term added in the
+// even-odd domain before the recombination (KronParams::Ft packing: Fe, Fo, Fm); both sides
+// cost n NL FMAs per line
+template <int N, int NL, typename T>
+__device__ __forceinline__ void face_eo(const T* __restrict__ F, const T (&gm)[NL], const T (&gp)[NL], int i,
+                                        T& ye, T& yo) {
+  constexpr int H = N / 2;
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    ye = fma(F[i * NL + l], gm[l] + gp[NL - 1 - l], ye);
+    yo = fma(F[H * NL + i * NL + l], gm[l] - gp[NL - 1 - l], yo);
+  }
+}
+template <int N, int NL, typename T>
+__device__ __forceinline__ void face_mid(const T* __restrict__ F, const T (&gm)[NL], const T (&gp)[NL], T& ym) {
+  constexpr int H = N / 2;
+#pragma unroll
+  for (int l = 0; l < NL; ++l) ym = fma(F[2 * H * NL + l], gm[l] + gp[NL - 1 - l], ym);
+}
+template <int N, int NL, typename T>
+__device__ __forceinline__ void eo_mul_f(const T* __restrict__ A, const EOSplit<N, T>& s, const T* __restrict__ F,
+                                         const T (&gm)[NL], const T (&gp)[NL], T (&y)[N]) {
+  constexpr int H = N / 2;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    T ye = T(0), yo = T(0);
+    if (N & 1) ye = A[2 * H * H + i] * s.m;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      ye = fma(A[i * H + j], s.e[j], ye);
+      yo = fma(A[H * H + i * H + j], s.o[j], yo);
+    }
+    face_eo<N, NL>(F, gm, gp, i, ye, yo);
+    y[i] = ye + yo;
+    y[N - 1 - i] = ye - yo;
+  }
+  if (N & 1) {
+    const T* Rw = A + 2 * H * H + H;
+    T ym = Rw[H] * s.m;
+#pragma unroll
+    for (int j = 0; j < H; ++j) ym = fma(Rw[j], s.e[j], ym);
+    face_mid<N, NL>(F, gm, gp, ym);
+    y[H] = ym;
+  }
+}
+template <int N, int NL, typename T>
+__device__ __forceinline__ void eo_mul2_f(const T* __restrict__ A1, const EOSplit<N, T>& s1,
+                                          const T* __restrict__ A2, const EOSplit<N, T>& s2,
+                                          const T* __restrict__ F, const T (&gm)[NL], const T (&gp)[NL],
+                                          T (&y)[N]) {
+  constexpr int H = N / 2;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    T ye = T(0), yo = T(0);
+    if (N & 1) ye = fma(A2[2 * H * H + i], s2.m, A1[2 * H * H + i] * s1.m);
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      ye = fma(A1[i * H + j], s1.e[j], ye);
+      yo = fma(A1[H * H + i * H + j], s1.o[j], yo);
+    }
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      ye = fma(A2[i * H + j], s2.e[j], ye);
+      yo = fma(A2[H * H + i * H + j], s2.o[j], yo);
+    }
+    face_eo<N, NL>(F, gm, gp, i, ye, yo);
+    y[i] = ye + yo;
+    y[N - 1 - i] = ye - yo;
+  }
+  if (N & 1) {
+    const T* R1 = A1 + 2 * H * H + H;
+    const T* R2 = A2 + 2 * H * H + H;
+    T ym = fma(R2[H], s2.m, R1[H] * s1.m);
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      ym = fma(R1[j], s1.e[j], ym);
+      ym = fma(R2[j], s2.e[j], ym);
+    }
+    face_mid<N, NL>(F, gm, gp, ym);
+    y[H] = ym;
+  }
+}
+
 // P^{-1} building blocks of the fused Chebyshev step: GL-Jacobi (Eq. (12)) or FDM
 template <int N, int MODE, typename KP, typename T>
 __device__ __forceinline__ void pinv_pre(const KP& kp, const T (&v)[N], T (&o)[N]) {
@@ -242,7 +325,10 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
   constexpr Lay3 LZY = Lay::ZY, LYX = Lay::YX, LXZ = Lay::XZ, LOUT = Lay::OUT;
   // R lines swept together (K4_RLINE): measured +2.5-3 % for the n = 4 Chebyshev step, -3..-5 %
   // at n = 5 (more live registers), n = 7 spills at its register cap; so n = 4 only
-  constexpr bool kRL = K4_RLINE && R > 1 && N == 4;
+  // KMODE_CHEBY_GLT: the matvec stages use T^{-T}-premultiplied factors (kp.Mt, kp.Lt, kp.Ft)
+  constexpr bool kT = MODE == KMODE_CHEBY_GLT;
+  constexpr bool kRL = K4_RLINE && R > 1 && N == 4 && !kT;
+  const Real* cM = kT ? kp.Mt : kp.M;
   constexpr int PG = Lay::PG, GPG = Lay::GPG, GFS = Lay::GFS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real* smem = reinterpret_cast<Real*>(smem_raw);
@@ -442,10 +528,14 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
       }
       Real t[N], a[N];
       const auto su = eo_split<N>(uz);
-      eo_mul<N, 1, false>(kp.M, su, t);
-      eo_mul<N, 1, false>(kp.L[2], su, a);
-      dense_add<NL, NL>(kp.Nm[2], zm, &a[0]);
-      dense_add<NL, NL>(kp.Np[2], zp, &a[N - NL]);
+      eo_mul<N, 1, false>(cM, su, t);
+      if constexpr (kT) {
+        eo_mul_f<N, NL>(kp.Lt[2], su, kp.Ft[2], zm, zp, a);
+      } else {
+        eo_mul<N, 1, false>(kp.L[2], su, a);
+        dense_add<NL, NL>(kp.Nm[2], zm, &a[0]);
+        dense_add<NL, NL>(kp.Np[2], zp, &a[N - NL]);
+      }
       Real* T = R1 + cslot * LZY.CS;
       Real* A = R2 + cslot * LZY.CS;
 #pragma unroll
@@ -457,7 +547,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
   }
   if (jsrc) {
     Real o[N];
-    eo_apply<N, 1>(kp.M, jv, o);
+    eo_apply<N, 1>(cM, jv, o);
 #pragma unroll
     for (int k = 0; k < N; ++k) jdst[k * jds] = o[k];
   }
@@ -467,7 +557,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
     Real* dst;
     int ds = PG;
     job_target(job, src, dst, ds);
-    if (src) mass_line<N>(kp.M, src, NN, dst, ds);
+    if (src) mass_line<N>(cM, src, NN, dst, ds);
   }
   __syncthreads();
 
@@ -525,10 +615,15 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
           gyp[l] = yp_row >= 0 ? GY[(1 * NL + l) * GFS + yk * GPG + yi] : -tl[N - 1 - l];
         }
         const auto st = eo_split<N>(tl);
-        eo_mul2<N, 1>(kp.M, eo_split<N>(al), kp.L[1], st, bl[r]);
-        eo_mul<N, 1, false>(kp.M, st, cl[r]);
-        dense_add<NL, NL>(kp.Nm[1], gym, &bl[r][0]);
-        dense_add<NL, NL>(kp.Np[1], gyp, &bl[r][N - NL]);
+        if constexpr (kT) {
+          eo_mul2_f<N, NL>(kp.Mt, eo_split<N>(al), kp.Lt[1], st, kp.Ft[1], gym, gyp, bl[r]);
+          eo_mul<N, 1, false>(kp.Mt, st, cl[r]);
+        } else {
+          eo_mul2<N, 1>(kp.M, eo_split<N>(al), kp.L[1], st, bl[r]);
+          eo_mul<N, 1, false>(kp.M, st, cl[r]);
+          dense_add<NL, NL>(kp.Nm[1], gym, &bl[r][0]);
+          dense_add<NL, NL>(kp.Np[1], gyp, &bl[r][N - NL]);
+        }
       }
     }
     {   // halo jobs: HC[h][l][k][j] = M_y HT[h][l][k][:], spread over the block
@@ -537,7 +632,7 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
         const int h = job < nh0 ? 0 : 1;
         const int q = job - (h ? nh0 : 0);
         const int l = q / N, k = q - l * N;
-        mass_line<N>(kp.M, HX + (((h * 2 + 0) * NL + l) * N + k) * PG, 1,
+        mass_line<N>(cM, HX + (((h * 2 + 0) * NL + l) * N + k) * PG, 1,
                      HX + (((h * 2 + 1) * NL + l) * N + k) * PG, 1);
       }
     }
@@ -657,9 +752,13 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
         cxp[l] = slot_p ? Cf[offp + at(LYX, Lp, xj, xk)]
                         : (need_h1 ? HX[(((1 * 2 + 1) * NL + l) * N + xk) * PG + xj] : -cl[N - 1 - Lp]);
       }
-      eo_mul2<N, 1>(kp.M, eo_split<N>(bl), kp.L[0], eo_split<N>(cl), res[r]);
-      dense_add<NL, NL>(kp.Nm[0], cxm, &res[r][0]);
-      dense_add<NL, NL>(kp.Np[0], cxp, &res[r][N - NL]);
+      if constexpr (kT) {
+        eo_mul2_f<N, NL>(kp.Mt, eo_split<N>(bl), kp.Lt[0], eo_split<N>(cl), kp.Ft[0], cxm, cxp, res[r]);
+      } else {
+        eo_mul2<N, 1>(kp.M, eo_split<N>(bl), kp.L[0], eo_split<N>(cl), res[r]);
+        dense_add<NL, NL>(kp.Nm[0], cxm, &res[r][0]);
+        dense_add<NL, NL>(kp.Np[0], cxp, &res[r][N - NL]);
+      }
     }
     }
   }
@@ -732,6 +831,98 @@ k_kron4(const __grid_constant__ KronParamsT<Real> kp, const __grid_constant__ Gr
           for (int i = 0; i < N; ++i) res[r][i] = ldsrc<kStage>(bb + i) - res[r][i];
         }
       }
+    }
+    if constexpr (kT) {
+      // transformed residual r~ = b~ - (T^{-T})^{(x)3} A u on the x-lines: P^{-1} r = (T^{-1})^{(x)3}
+      // diag(A_GL)^{-1} r~ as x: diag, T^{-1}; y: T^{-1}; z: T^{-1} + the update of Eq. (11)
+      Real dl[R][N];
+      if (active) {   // the x-line diagonal, issued before the barrier
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int xb = tb + r * NB;
+          if (N % R != 0 && xb >= N) break;
+          const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
+          const Real* dv = ch.dinv + cid * N3 + (xk * N + xj) * N;
+          if constexpr (N % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < N; i += 2) {
+              const V2 d2 = __ldg(reinterpret_cast<const V2*>(dv + i));
+              dl[r][i] = d2.x;
+              dl[r][i + 1] = d2.y;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < N; ++i) dl[r][i] = __ldg(dv + i);
+          }
+        }
+      }
+      __syncthreads();   // B, C fully read (C also by the neighbour slots)
+      if (active) {   // x: diag, T^{-1} -> R2 (x-write / y-read)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int xb = tb + r * NB;
+          if (N % R != 0 && xb >= N) break;
+          const int xj = XSW ? xb : ta, xk = XSW ? ta : xb;
+          Real v[N], o[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) v[i] = res[r][i] * dl[r][i];
+          eo_apply<N, 1>(kp.Ti, v, o);
+          Real* W = R2 + cslot * LYX.CS;
+#pragma unroll
+          for (int i = 0; i < N; ++i) W[at(LYX, i, xj, xk)] = o[i];
+        }
+      }
+      __syncthreads();
+      Real ujz[R][N], upz[R][N];   // the update's inputs along the z-lines, loaded one stage early
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int zj = tb + r * NB, zi = ta;
+          if (N % R != 0 && zj >= N) break;
+          const int64_t gbase = cid * N3 + zj * N + zi;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            ujz[r][k] = __ldg(u + gbase + k * NN);
+            if (!ch.first) upz[r][k] = __ldg(ch.u_prev + gbase + k * NN);
+          }
+        }
+      }
+      if (active) {   // y: T^{-1} -> R1 (y-write / z-read)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int yk = tb + r * NB, yi = ta;
+          if (N % R != 0 && yk >= N) break;
+          const Real* Rd = R2 + cslot * LYX.CS;
+          Real* W = R1 + cslot * LZY.CS;
+          Real v[N], o[N];
+#pragma unroll
+          for (int j = 0; j < N; ++j) v[j] = Rd[at(LYX, yi, j, yk)];
+          eo_apply<N, 1>(kp.Ti, v, o);
+#pragma unroll
+          for (int j = 0; j < N; ++j) W[at(LZY, yi, j, yk)] = o[j];
+        }
+      }
+      __syncthreads();
+      if (active) {   // z: T^{-1}, three-term update (Eq. (11)) along the z-lines
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int zj = tb + r * NB, zi = ta;
+          if (N % R != 0 && zj >= N) break;
+          const Real* Rd = R1 + cslot * LZY.CS;
+          Real v[N], z[N];
+#pragma unroll
+          for (int k = 0; k < N; ++k) v[k] = Rd[at(LZY, zi, zj, k)];
+          eo_apply<N, 1>(kp.Ti, v, z);
+          const int64_t gbase = cid * N3 + zj * N + zi;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            Real vv = fma((Real)ch.c_z, z[k], ujz[r][k]);
+            if (!ch.first) vv = fma((Real)ch.c_prev, ujz[r][k] - upz[r][k], vv);
+            ch.u_next[gbase + k * NN] = vv;
+          }
+        }
+      }
+      return;
     }
     __syncthreads();   // B, C fully read (C also by the neighbour slots)
     if constexpr ((MODE == KMODE_CHEBY_GL || MODE == KMODE_CHEBY_FDM) && N % 2 == 0) {
@@ -1051,6 +1242,15 @@ cudaError_t launch_t(const KronParamsT<Real>& kp, const GridArgs& g, const Real*
   return cudaGetLastError();
 }
 
+// KMODE_CHEBY_GLT exists for fp64 and NL = 2 only (KronParams::Ft is packed for NL = 2)
+template <int N, int NL, int OUTD, int ALT, typename Real>
+cudaError_t launch_glt(const KronParamsT<Real>& kp, const GridArgs& g, const Real* u, Real* y,
+                       const ChebyArgsT<Real>& ch, cudaStream_t s) {
+  if constexpr (std::is_same<Real, double>::value && NL == 2)
+    return launch_t<N, NL, KMODE_CHEBY_GLT, OUTD, ALT, Real>(kp, g, u, y, ch, s);
+  return cudaErrorInvalidValue;
+}
+
 template <int N, int NL, typename Real>
 cudaError_t launch_mode(int mode, const KronParamsT<Real>& kp, const GridArgs& g, const Real* u, Real* y,
                         const ChebyArgsT<Real>& ch, cudaStream_t s) {
@@ -1073,6 +1273,7 @@ cudaError_t launch_mode(int mode, const KronParamsT<Real>& kp, const GridArgs& g
         case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 2, Real>(kp, g, u, y, ch, s);
         case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 2, Real>(kp, g, u, y, ch, s);
         case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_GLT: return launch_glt<N, NL, 0, 2, Real>(kp, g, u, y, ch, s);
       }
       return cudaErrorInvalidValue;
     }
@@ -1088,6 +1289,7 @@ cudaError_t launch_mode(int mode, const KronParamsT<Real>& kp, const GridArgs& g
         case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 2, Real>(kp, g, u, y, ch, s);
         case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 2, Real>(kp, g, u, y, ch, s);
         case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_GLT: return launch_glt<N, NL, 0, 2, Real>(kp, g, u, y, ch, s);
       }
       return cudaErrorInvalidValue;
     }
@@ -1103,6 +1305,7 @@ cudaError_t launch_mode(int mode, const KronParamsT<Real>& kp, const GridArgs& g
         case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 2, Real>(kp, g, u, y, ch, s);
         case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 2, Real>(kp, g, u, y, ch, s);
         case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 2, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_GLT: return launch_glt<N, NL, 0, 2, Real>(kp, g, u, y, ch, s);
       }
       return cudaErrorInvalidValue;
     }
@@ -1116,6 +1319,7 @@ cudaError_t launch_mode(int mode, const KronParamsT<Real>& kp, const GridArgs& g
         case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 1, Real>(kp, g, u, y, ch, s);
         case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 1, Real>(kp, g, u, y, ch, s);
         case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 1, Real>(kp, g, u, y, ch, s);
+        case KMODE_CHEBY_GLT: return launch_glt<N, NL, 0, 1, Real>(kp, g, u, y, ch, s);
       }
       return cudaErrorInvalidValue;
     }
@@ -1127,6 +1331,7 @@ cudaError_t launch_mode(int mode, const KronParamsT<Real>& kp, const GridArgs& g
     case KMODE_CHEBY_GL: return launch_t<N, NL, KMODE_CHEBY_GL, 0, 0, Real>(kp, g, u, y, ch, s);
     case KMODE_CHEBY_PJ: return launch_t<N, NL, KMODE_CHEBY_PJ, 0, 0, Real>(kp, g, u, y, ch, s);
     case KMODE_CHEBY_FDM: return launch_t<N, NL, KMODE_CHEBY_FDM, 0, 0, Real>(kp, g, u, y, ch, s);
+    case KMODE_CHEBY_GLT: return launch_glt<N, NL, 0, 0, Real>(kp, g, u, y, ch, s);
   }
   return cudaErrorInvalidValue;
 }

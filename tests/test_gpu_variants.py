@@ -32,6 +32,8 @@ VARIANTS = [
     ({"DG_K6": "255", "DG_K3C": "0"}, "2,3,4,5", False),   # k_kron6 i-plane matvec + Chebyshev for n = 3..6
     ({"DG_K6": "0", "DG_K3C": "0"}, "2,3,4,5", False),     # k_kron4 for every n
     ({"DG_L2PF": "0", "DG_K3C": "1"}, "2", False),          # k_kron3c (the n = 3 default) without L2 prefetch
+    ({"DG_CHEBY_GLT": "0"}, "3,4", False),     # the direct GL-Jacobi step (no transformed residual)
+    ({"DG_CHEBY_GLT": "9", "DG_K3C": "0"}, "2,5", False),   # transformed-residual step at n = 3 and 6 (bits n-3)
 ]
 
 

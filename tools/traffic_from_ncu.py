@@ -5,7 +5,7 @@
       python bench.py --steps 1 --warmup 0 --quick > traffic.csv
   python tools/traffic_from_ncu.py traffic.csv profiles/rN_traffic.json profiles/rN_traffic_ncu.csv
 
-Per degree p (template n = p+1) and mode (0 = APPLY, 1 = CHEBY_GL) the median DRAM
+Per degree p (template n = p+1) and mode (0 = APPLY, 1 = CHEBY_GL, 4 = CHEBY_GLT) the median DRAM
 bytes per launch are recorded next to the algorithmic bytes (16 / 40 B per DoF).
 """
 import csv
@@ -42,7 +42,7 @@ for r in rows:
         nl, kern = 2, "k_kron6"
     else:
         continue
-    if nl != 2 or mode not in (0, 1):
+    if nl != 2 or mode not in (0, 1, 4):
         continue
     key = (n - 1, mode, kern)
     per.setdefault(key, {}).setdefault(r[idi], {})[r[mi]] = float(r[vi].replace(",", ""))
@@ -50,7 +50,7 @@ out = {"c4": {}}
 src = sys.argv[3] if len(sys.argv) > 3 else sys.argv[1]
 for (p, mode, kern), launches in sorted(per.items()):
     tot = [v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in launches.values()]
-    name = f"{kern}<APPLY>" if mode == 0 else f"{kern}<CHEBY_GL>"
+    name = f"{kern}<" + {0: "APPLY", 1: "CHEBY_GL", 4: "CHEBY_GLT"}[mode] + ">"
     ent = out["c4"].setdefault(name, {"per_launch_bytes": {}, "algorithmic_bytes": {}, "launches": {},
                                       "source": src})
     nd = c4_spec(p).n_dofs
