@@ -476,7 +476,8 @@ def run_ours(a, rank, world, local_rank):
         kname = "k_quad3"
     else:
         kname = "k_quad"
-    bname = "k_bchg4" if os.environ.get("DG_BCHG") == "4" else "k_bchg"   # k_bchg4 default only at p=2, 8
+    # default: the warp-private pipelined k_bchgw at p = 2, 4, 5, 6, 8 (n = 3, 5, 6, 7, 9), k_bchg at p = 3, 7
+    bname = {"4": "k_bchg4", "5": "k_bchgw", "1": "k_bchg"}.get(os.environ.get("DG_BCHG", ""), "k_bchgw/k_bchg")
     kernel = {"matvec": f"{kname}<APPLY>", "basis_change": bname,
               "chebyshev_step": f"{kname}<CHEBY_GL>"}[dom_name]
     kper = {q: kernel for q in degrees}

@@ -1039,15 +1039,19 @@ dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, 
   BchgParams bp{};
   pack_eo(B, n, bp.B);
   cudaStream_t s = (cudaStream_t)stream;
-  // k_bchg (cell-staged, in-place capable) or the z-first k_bchg4 (out of place only).
-  // Default by measurement (C4, tools/bchg_ab.py): k_bchg4 for n = 3 and 9, k_bchg otherwise;
-  // DG_BCHG=1 / DG_BCHG=4 force one of them.
+  // Three kernels: k_bchg (block-staged), the z-first k_bchg4 (out of place only) and the
+  // warp-private pipelined k_bchgw.  Default by measurement (C4, tools/gpu_bchgw.sh, GB/s at
+  // p = 2..8: k_bchg 4245/5869/4736/4925/4435/5855/4853, k_bchg4 4477/5188/4185/4856/4186/4471/5231,
+  // k_bchgw in its best mode 5537/5893/5843/5372/4633/5087/5923): k_bchgw for n = 3, 5, 6, 7, 9,
+  // k_bchg otherwise; DG_BCHG=1 / 4 / 5 force one of them.
   static const int v = [] {
     const char* e = std::getenv("DG_BCHG");
     return e ? std::atoi(e) : 0;
   }();
-  const bool use4 = v == 4 || (v == 0 && (n == 3 || n == 9));
-  if (use4 && in != out && kron4_supported(n))
+  const bool usew = v == 5 || (v == 0 && (n == 3 || n == 5 || n == 6 || n == 7 || n == 9));
+  if (usew)
+    return post_launch(m, launch_basis_change_w(n, bp, in, out, m->ncells_local, s), "basis_change", s);
+  if (v == 4 && in != out && kron4_supported(n))
     return post_launch(m, launch_basis_change4(n, bp, in, out, m->ncells_local, s), "basis_change", s);
   return post_launch(m, launch_basis_change(n, bp, in, out, m->ncells_local, s), "basis_change", s);
 }
@@ -1071,6 +1075,12 @@ dg_status dg_basis_change_f32(dg_mesh m, int32_t op, const float* in, float* out
   BchgParamsF bf{};
   for (int k = 0; k < kEO; ++k) bf.B[k] = (float)bp.B[k];
   cudaStream_t s = (cudaStream_t)stream;
+  static const int v = [] {
+    const char* e = std::getenv("DG_BCHG");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (v == 5)
+    return post_launch(m, launch_basis_change_w_f32(n, bf, in, out, m->ncells_local, s), "basis_change_f32", s);
   return post_launch(m, launch_basis_change_f32(n, bf, in, out, m->ncells_local, s), "basis_change_f32", s);
 }
 

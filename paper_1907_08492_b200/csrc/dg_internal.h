@@ -159,6 +159,11 @@ cudaError_t launch_basis_change(int n, const BchgParams& bp, const double* in, d
                                 int64_t ncells, cudaStream_t s);
 cudaError_t launch_basis_change_f32(int n, const BchgParamsF& bp, const float* in, float* out,
                                     int64_t ncells, cudaStream_t s);
+// warp-private pipelined basis change (k_bchgw.cu), in-place capable
+cudaError_t launch_basis_change_w(int n, const BchgParams& bp, const double* in, double* out,
+                                  int64_t ncells, cudaStream_t s);
+cudaError_t launch_basis_change_w_f32(int n, const BchgParamsF& bp, const float* in, float* out,
+                                      int64_t ncells, cudaStream_t s);
 // diagonal of a Cartesian Kronecker operator: d[i,j,k] = sum_d c_d prod(1D diagonals)
 struct CartDiagParams {
   double mdiag[kMaxN];                 // diag(Mhat_basis)

@@ -45,3 +45,29 @@ def test_variant_parity(env, degrees, curved):
     cmd = [sys.executable, os.path.join(HERE, "_variant_check.py"), degrees] + (["curved"] if curved else [])
     r = subprocess.run(cmd, env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+# Basis change (a12): the three kernels (DG_BCHG = 1 block-staged k_bchg, 4 z-first k_bchg4 via
+# _variant_check above, 5 warp-private pipelined k_bchgw in its four modes) and the per-n
+# default mix, each at p = 1..8, all four ops, in place and out of place, fp64 and fp32
+# (tests/_bchg_check.py).  DG_BCHGW_GRID=2 makes every warp stream many tiles through its slots.
+BCHG_VARIANTS = [
+    {"DG_BCHG": "5", "DG_BCHGW_MODE": "0", "DG_BCHGW_GRID": "2"},
+    {"DG_BCHG": "5", "DG_BCHGW_MODE": "1", "DG_BCHGW_GRID": "2"},
+    {"DG_BCHG": "5", "DG_BCHGW_MODE": "2", "DG_BCHGW_GRID": "2"},
+    {"DG_BCHG": "5", "DG_BCHGW_MODE": "3", "DG_BCHGW_GRID": "2"},
+    {"DG_BCHG": "5"},
+    {"DG_BCHG": "1"},
+    {"DG_BCHGW_GRID": "2"},
+    {},
+]
+
+
+@pytest.mark.parametrize("env", BCHG_VARIANTS,
+                         ids=[",".join(f"{k}={v}" for k, v in e.items()) or "default" for e in BCHG_VARIANTS])
+def test_basis_change_kernels(env):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cmd = [sys.executable, os.path.join(HERE, "_bchg_check.py")]
+    r = subprocess.run(cmd, env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
