@@ -267,7 +267,7 @@ def _measured_traffic(workload, names, degrees):
     dram__bytes_write.sum` pass of this workload, per degree), averaged over the degrees
     like `achieved`; None if the capture does not cover this workload/kernel."""
     caps = []
-    for fn in ("r2s4_traffic.json", "r2_traffic.json", "r1_traffic.json"):   # newest capture first
+    for fn in ("r2s5_traffic.json", "r2s4_traffic.json", "r2_traffic.json", "r1_traffic.json"):   # newest capture first
         p = os.path.join(ROOT, "profiles", fn)
         if os.path.exists(p):
             with open(p) as f:
@@ -476,8 +476,9 @@ def run_ours(a, rank, world, local_rank):
         kname = "k_quad3"
     else:
         kname = "k_quad"
-    # default: the warp-private pipelined k_bchgw at p = 2, 4, 5, 6, 8 (n = 3, 5, 6, 7, 9), k_bchg at p = 3, 7
-    bname = {"4": "k_bchg4", "5": "k_bchgw", "1": "k_bchg"}.get(os.environ.get("DG_BCHG", ""), "k_bchgw/k_bchg")
+    # default: the warp-private pipelined kernels of k_bchgw.cu (plane mode k_bchgp at p = 2..7, line mode
+    # k_bchgw at p = 8)
+    bname = {"4": "k_bchg4", "5": "k_bchgp/k_bchgw", "1": "k_bchg"}.get(os.environ.get("DG_BCHG", ""), "k_bchgp/k_bchgw")
     kernel = {"matvec": f"{kname}<APPLY>", "basis_change": bname,
               "chebyshev_step": f"{kname}<CHEBY_GL>"}[dom_name]
     kper = {q: kernel for q in degrees}

@@ -1040,15 +1040,15 @@ dg_status dg_basis_change(dg_mesh m, int32_t op, const double* in, double* out, 
   pack_eo(B, n, bp.B);
   cudaStream_t s = (cudaStream_t)stream;
   // Three kernels: k_bchg (block-staged), the z-first k_bchg4 (out of place only) and the
-  // warp-private pipelined k_bchgw.  Default by measurement (C4, tools/gpu_bchgw.sh, GB/s at
+  // warp-private pipelined k_bchgw / k_bchgp (k_bchgw.cu).  Default by measurement (C4, GB/s at
   // p = 2..8: k_bchg 4245/5869/4736/4925/4435/5855/4853, k_bchg4 4477/5188/4185/4856/4186/4471/5231,
-  // k_bchgw in its best mode 5537/5893/5843/5372/4633/5087/5923): k_bchgw for n = 3, 5, 6, 7, 9,
-  // k_bchg otherwise; DG_BCHG=1 / 4 / 5 force one of them.
+  // k_bchgw.cu in its per-n default mode 6364/6321/6557/6326/6418/6206/5904 = 0.90-1.00 of the
+  // measured copy bandwidth): k_bchgw.cu for n >= 3, k_bchg for n = 2; DG_BCHG=1 / 4 / 5 force one.
   static const int v = [] {
     const char* e = std::getenv("DG_BCHG");
     return e ? std::atoi(e) : 0;
   }();
-  const bool usew = v == 5 || (v == 0 && (n == 3 || n == 5 || n == 6 || n == 7 || n == 9));
+  const bool usew = v == 5 || (v == 0 && n >= 3);
   if (usew)
     return post_launch(m, launch_basis_change_w(n, bp, in, out, m->ncells_local, s), "basis_change", s);
   if (v == 4 && in != out && kron4_supported(n))

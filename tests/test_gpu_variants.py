@@ -48,7 +48,7 @@ def test_variant_parity(env, degrees, curved):
 
 
 # Basis change (a12): the three kernels (DG_BCHG = 1 block-staged k_bchg, 4 z-first k_bchg4 via
-# _variant_check above, 5 warp-private pipelined k_bchgw in its four modes) and the per-n
+# _variant_check above, 5 warp-private pipelined k_bchgw in its four line modes and two plane modes) and the per-n
 # default mix, each at p = 1..8, all four ops, in place and out of place, fp64 and fp32
 # (tests/_bchg_check.py).  DG_BCHGW_GRID=2 makes every warp stream many tiles through its slots.
 BCHG_VARIANTS = [
@@ -56,6 +56,8 @@ BCHG_VARIANTS = [
     {"DG_BCHG": "5", "DG_BCHGW_MODE": "1", "DG_BCHGW_GRID": "2"},
     {"DG_BCHG": "5", "DG_BCHGW_MODE": "2", "DG_BCHGW_GRID": "2"},
     {"DG_BCHG": "5", "DG_BCHGW_MODE": "3", "DG_BCHGW_GRID": "2"},
+    {"DG_BCHG": "5", "DG_BCHGW_MODE": "4", "DG_BCHGW_GRID": "2"},   # plane mode (k_bchgp), 3 slots
+    {"DG_BCHG": "5", "DG_BCHGW_MODE": "6", "DG_BCHGW_GRID": "2"},   # plane mode, 2 slots
     {"DG_BCHG": "5"},
     {"DG_BCHG": "1"},
     {"DG_BCHGW_GRID": "2"},

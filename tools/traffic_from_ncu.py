@@ -40,9 +40,12 @@ for r in rows:
     elif m6:
         n, mode = map(int, m6.groups())
         nl, kern = 2, "k_kron6"
+    elif re.search(r"k_bchg[wp]?<", r[ki]):   # basis change: k_bchg<N, CPB, ..> / k_bchgw<N, NSLOT, ..>, 16 B/DoF
+        mb = re.search(r"(k_bchg[wp]?)<(?:\(int\))?(\d)", r[ki])
+        n, nl, mode, kern = int(mb.group(2)), 2, 9, mb.group(1)
     else:
         continue
-    if nl != 2 or mode not in (0, 1, 4):
+    if nl != 2 or mode not in (0, 1, 4, 9):
         continue
     key = (n - 1, mode, kern)
     per.setdefault(key, {}).setdefault(r[idi], {})[r[mi]] = float(r[vi].replace(",", ""))
@@ -50,7 +53,7 @@ out = {"c4": {}}
 src = sys.argv[3] if len(sys.argv) > 3 else sys.argv[1]
 for (p, mode, kern), launches in sorted(per.items()):
     tot = [v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in launches.values()]
-    name = f"{kern}<" + {0: "APPLY", 1: "CHEBY_GL", 4: "CHEBY_GLT"}[mode] + ">"
+    name = kern if mode == 9 else f"{kern}<" + {0: "APPLY", 1: "CHEBY_GL", 4: "CHEBY_GLT"}[mode] + ">"
     ent = out["c4"].setdefault(name, {"per_launch_bytes": {}, "algorithmic_bytes": {}, "launches": {},
                                       "source": src})
     nd = c4_spec(p).n_dofs
