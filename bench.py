@@ -485,7 +485,7 @@ def run_ours(a, rank, world, local_rank):
     k3c = os.environ.get("DG_K3C", "1") != "0"
     if cart and dom_name == "chebyshev_step":
         # transformed-residual step (KMODE_CHEBY_GLT) where bit n-3 of DG_CHEBY_GLT is set (the
-        # library's default mask 0x77: every n but 6), after one k_bchg pass b~ = (T^-T)^(x)3 b per sweep
+        # library's default mask 0x77: every n but 6), after one basis-change pass b~ = (T^-T)^(x)3 b per sweep
         glt = int(os.environ.get("DG_CHEBY_GLT", "119"))
         for q in degrees:
             if (glt >> (q - 2)) & 1 and not (q == 2 and k3c):
@@ -493,7 +493,7 @@ def run_ours(a, rank, world, local_rank):
         gq = [q for q in degrees if kper[q].endswith("GLT>")]
         if gq:
             dq = [q for q in degrees if q not in gq and not (q == 2 and k3c)]
-            kernel = (f"k_kron4<CHEBY_GLT> (p={','.join(map(str, gq))}; + one k_bchg pass per sweep)"
+            kernel = (f"k_kron4<CHEBY_GLT> (p={','.join(map(str, gq))}; + one basis-change pass per sweep)"
                       + (f" + k_kron4<CHEBY_GL> (p={','.join(map(str, dq))})" if dq else ""))
     if cart and dom_name != "basis_change" and 2 in degrees and k3c:
         kper[2] = f"k_kron3c<{'APPLY' if dom_name == 'matvec' else 'CHEBY_GL'}>"
@@ -505,7 +505,7 @@ def run_ours(a, rank, world, local_rank):
                 "per_degree_frac": {k: (o["cheby_frac_hbm"] if dom_name == "chebyshev_step" else o["matvec_frac_hbm"])
                                     for k, o in ops.items()},
                 "note": "achieved = algorithmic bytes (matvec/basis change 16 B/DoF, Chebyshev step "
-                        "40 B/DoF, first step 32; the transformed-residual sweep's extra k_bchg pass on b "
+                        "40 B/DoF, first step 32; the transformed-residual sweep's extra basis-change pass on b "
                         "is not counted) / summed CUDA-event time of that op, per GPU"}
     mv_gbs = dom["matvec"][0] / (dom["matvec"][1] * 1e-3) / 1e9 / world
     matvec_roof = {"achieved_gbs": mv_gbs, "frac_hbm": mv_gbs / hbm_peak}

@@ -1079,7 +1079,9 @@ dg_status dg_basis_change_f32(dg_mesh m, int32_t op, const float* in, float* out
     const char* e = std::getenv("DG_BCHG");
     return e ? std::atoi(e) : 0;
   }();
-  if (v == 5)
+  // fp32 default by measurement (C4, GB/s at 8 B/DoF, p = 2..8: k_bchg 2993/4419/3908/3475/3489/4941/3844,
+  // k_bchgw.cu plane mode with two slots 5150/3281/5014/3953/4994/5045/4560): k_bchg at n = 2 and 4
+  if (v == 5 || (v == 0 && n >= 3 && n != 4))
     return post_launch(m, launch_basis_change_w_f32(n, bf, in, out, m->ncells_local, s), "basis_change_f32", s);
   return post_launch(m, launch_basis_change_f32(n, bf, in, out, m->ncells_local, s), "basis_change_f32", s);
 }

@@ -371,28 +371,29 @@ cudaError_t launch_cfg(const BP& bp, const Real* in, Real* out, int64_t ncells, 
   void (*kern)(BP, const Real*, Real*, int64_t, int64_t);
   if constexpr (PLANE) kern = k_bchgp<N, NSLOT, Real, BP>;
   else kern = k_bchgw<N, NSLOT, ZD, Real, BP>;
-  static int grid_cap = 0;     // SMs x resident blocks, found once per instantiation
-  if (!grid_cap) {
+  // SMs x resident blocks (> 0) or minus the CUDA error, found once per instantiation
+  // (thread-safe static: the slab-transport tests call this from several host threads)
+  static const int grid_cap = [&]() -> int {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) return -(int)e;
     int dev = 0, sms = 0, bps = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kBwWarps * 32, smem);
-    if (e != cudaSuccess) return e;
-    if (bps < 1) return cudaErrorLaunchOutOfResources;
+    if (e != cudaSuccess) return -(int)e;
+    if (bps < 1 || sms < 1) return -(int)cudaErrorLaunchOutOfResources;
     // blocks per SM: DG_BCHGW_BPS, else one block (4 warps) in plane mode at n = 4 and 6, where more
     // resident warps measured slower (n = 4: 6321 vs 5836 GB/s, n = 6: 6326 vs 5802)
-    static const int cap = [] {
-      const char* v = std::getenv("DG_BCHGW_BPS");
-      return v ? std::atoi(v) : ((PLANE && (N == 4 || N == 6)) ? 1 : 0);
-    }();
+    const char* v = std::getenv("DG_BCHGW_BPS");
+    const int cap = v ? std::atoi(v) : ((PLANE && (N == 4 || N == 6)) ? 1 : 0);
     if (cap > 0 && bps > cap) bps = cap;
-    grid_cap = sms * bps;
+    int grid = sms * bps;
     // DG_BCHGW_GRID: cap on the number of blocks (tests: many tiles per warp on small meshes)
     const char* g = std::getenv("DG_BCHGW_GRID");
-    if (g && std::atoi(g) > 0 && std::atoi(g) < grid_cap) grid_cap = std::atoi(g);
-  }
+    if (g && std::atoi(g) > 0 && std::atoi(g) < grid) grid = std::atoi(g);
+    return grid;
+  }();
+  if (grid_cap <= 0) return (cudaError_t)(-grid_cap);
   const int64_t ntiles = (ncells + TC - 1) / TC;
   int64_t blocks = (ntiles + kBwWarps - 1) / kBwWarps;
   if (blocks > grid_cap) blocks = grid_cap;
@@ -410,6 +411,7 @@ cudaError_t launch_n(const BP& bp, const Real* in, Real* out, int64_t ncells, cu
   static const int mode = [] {
     const char* v = std::getenv("DG_BCHGW_MODE");
     if (v) return std::atoi(v);
+    if (sizeof(Real) == 4) return 6;   // fp32 (8 B/DoF): plane mode, two slots (tools/gpu_bchg_misc.sh)
     return N == 9 ? 3 : (N == 6 ? 6 : 4);
   }();
   if constexpr (sizeof(Real) == 8) {
