@@ -15,7 +15,7 @@ for r in rows:
     m = re.search(r"(k_kron4)<(\d+), (\d+), (\d+)", name)
     m3 = re.search(r"(k_kron3c)<(\d+), (\d+)>", name)
     m6 = re.search(r"(k_kron6)<(\d+), (\d+)>", name)
-    mb = re.search(r"(k_bchg4?)<(\d+)", name)
+    mb = re.search(r"(k_bchg[4wp]?)<(?:\(int\))?(\d+)", name)
     if mb:
         key = f"{mb.group(1)}<n={mb.group(2)}>"
     elif m:

@@ -58,7 +58,7 @@ for (p, mode, kern), launches in sorted(per.items()):
                                       "source": src})
     nd = c4_spec(p).n_dofs
     ent["per_launch_bytes"][str(p)] = statistics.median(tot)
-    ent["algorithmic_bytes"][str(p)] = nd * (16.0 if mode == 0 else 40.0)
+    ent["algorithmic_bytes"][str(p)] = nd * (16.0 if mode in (0, 9) else 40.0)
     ent["launches"][str(p)] = len(tot)
 json.dump(out, open(sys.argv[2], "w"), indent=1)
 print(json.dumps(out, indent=1))
