@@ -285,7 +285,10 @@ dg_status dg_tables_1d(int32_t degree, int32_t basis, double penalty_factor, dou
  * kind 2: streaming read bandwidth in GB/s;
  * kind 3: fp64 tensor-core throughput in TFLOP/s (DMMA, mma.sync m8n8k4 f64 chains);
  * kind 4: DMMA chains and DFMA chains interleaved in one kernel, total TFLOP/s (if the two
- *         used separate pipes this would approach the sum of kinds 0 and 3).
+ *         used separate pipes this would approach the sum of kinds 0 and 3);
+ * kind 10 + n (n = 3..8): design probe, GDoF/s of a warp-private, cp.async-pipelined
+ *         plane-per-lane proxy of the Cartesian matvec's seven sweeps without neighbour terms
+ *         (csrc/k_probe_plane.cu; an upper bound for the schedule DESIGN.md §11 proposes).
  * Best of 5 timed launches. */
 dg_status dg_measure_peak(int32_t kind, double* value, void* stream);
 

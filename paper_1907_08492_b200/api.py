@@ -65,9 +65,12 @@ def get_nccl_unique_id() -> bytes:
 
 def measure_peak(kind: str, stream=None) -> float:
     """'fp64' -> TFLOP/s of DFMA; 'copy' / 'read' -> GB/s; 'dmma' -> fp64 tensor-core TFLOP/s;
-    'dmma+dfma' -> both interleaved (see dg_measure_peak)."""
+    'dmma+dfma' -> both interleaved; 'plane_probe_n<N>' (N = 3..8) -> GDoF/s of the pipelined-plane
+    matvec proxy (see dg_measure_peak)."""
     v = ctypes.c_double()
-    _check(lib().dg_measure_peak({"fp64": 0, "copy": 1, "read": 2, "dmma": 3, "dmma+dfma": 4}[kind], ctypes.byref(v),
+    kinds = {"fp64": 0, "copy": 1, "read": 2, "dmma": 3, "dmma+dfma": 4}
+    kinds.update({f"plane_probe_n{n}": 10 + n for n in range(3, 9)})
+    _check(lib().dg_measure_peak(kinds[kind], ctypes.byref(v),
                                  _stream(stream)), "dg_measure_peak")
     return v.value
 

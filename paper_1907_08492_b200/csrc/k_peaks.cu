@@ -83,7 +83,10 @@ __global__ void k_read(const double2* __restrict__ in, double* sink, int64_t n2)
 
 // kind 0: fp64 FMA TFLOP/s; 1: copy GB/s (read + write bytes); 2: read-only GB/s;
 // 3: fp64 tensor-core (DMMA) TFLOP/s; 4: DMMA and DFMA chains interleaved, total TFLOP/s
+cudaError_t measure_plane_probe(int n, double* value, cudaStream_t s);   // k_probe_plane.cu
+
 cudaError_t measure_peak(int kind, double* value, cudaStream_t s) {
+  if (kind >= 13 && kind <= 18) return measure_plane_probe(kind - 10, value, s);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

@@ -73,3 +73,18 @@ def test_basis_change_kernels(env):
     cmd = [sys.executable, os.path.join(HERE, "_bchg_check.py")]
     r = subprocess.run(cmd, env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_plane_probe_runs():
+    """The design probe of DESIGN.md §11 (dg_measure_peak kind 10 + n, csrc/k_probe_plane.cu) launches
+    and returns a finite positive rate; bad kinds are rejected."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1907_08492_b200 as P
+    v = P.measure_peak("plane_probe_n4")
+    assert v > 1.0 and v < 1e4
+    import ctypes
+    from paper_1907_08492_b200._lib import lib
+    x = ctypes.c_double()
+    assert lib().dg_measure_peak(9, ctypes.byref(x), None) != 0
+    assert lib().dg_measure_peak(19, ctypes.byref(x), None) != 0
