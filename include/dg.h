@@ -288,7 +288,8 @@ dg_status dg_tables_1d(int32_t degree, int32_t basis, double penalty_factor, dou
  *         used separate pipes this would approach the sum of kinds 0 and 3);
  * kind 10 + n (n = 3..8): design probe, GDoF/s of a warp-private, cp.async-pipelined
  *         plane-per-lane proxy of the Cartesian matvec's seven sweeps without neighbour terms
- *         (csrc/k_probe_plane.cu; an upper bound for the schedule DESIGN.md §11 proposes).
+ *         (csrc/k_probe_plane.cu; an upper bound for the schedule DESIGN.md §11 proposes);
+ * kind 20 + n (n = 3..6): the same probe with the neighbour-layer traffic and couplings.
  * Best of 5 timed launches. */
 dg_status dg_measure_peak(int32_t kind, double* value, void* stream);
 

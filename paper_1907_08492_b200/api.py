@@ -70,6 +70,7 @@ def measure_peak(kind: str, stream=None) -> float:
     v = ctypes.c_double()
     kinds = {"fp64": 0, "copy": 1, "read": 2, "dmma": 3, "dmma+dfma": 4}
     kinds.update({f"plane_probe_n{n}": 10 + n for n in range(3, 9)})
+    kinds.update({f"plane_probe_nb_n{n}": 20 + n for n in range(3, 7)})   # with neighbour traffic
     _check(lib().dg_measure_peak(kinds[kind], ctypes.byref(v),
                                  _stream(stream)), "dg_measure_peak")
     return v.value

@@ -975,7 +975,7 @@ dg_status dg_halo_set(dg_mesh m, const double* recv_lo, const double* recv_hi, v
 }
 
 dg_status dg_measure_peak(int32_t kind, double* value, void* stream) {
-  if (!value || kind < 0 || (kind > 4 && (kind < 13 || kind > 18))) return fail(DG_ERR_PARAM, "bad kind or NULL value");
+  if (!value || kind < 0 || (kind > 4 && (kind < 13 || kind > 18) && (kind < 23 || kind > 26))) return fail(DG_ERR_PARAM, "bad kind or NULL value");
   CUDA_TRY(measure_peak(kind, value, (cudaStream_t)stream));
   return DG_OK;
 }

@@ -87,6 +87,7 @@ cudaError_t measure_plane_probe(int n, double* value, cudaStream_t s);   // k_pr
 
 cudaError_t measure_peak(int kind, double* value, cudaStream_t s) {
   if (kind >= 13 && kind <= 18) return measure_plane_probe(kind - 10, value, s);
+  if (kind >= 23 && kind <= 26) return measure_plane_probe(kind - 10, value, s);   // with neighbour traffic
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

@@ -1,4 +1,5 @@
-// Design probe (dg_measure_peak kinds 13..18 = 10 + n, not a product kernel): an upper bound
+// Design probe (dg_measure_peak kinds 13..18 = 10 + n and, with neighbour traffic, 23..26 = 20 + n;
+// not a product kernel): an upper bound
 // for the matvec schedule DESIGN.md §11 proposes for n >= 4 -- k_kron6's i-plane arithmetic on
 // k_bchgp's skeleton (warp-private cp.async tile slots two stages ahead, no block barrier).
 // It performs the Cartesian matvec's seven 1D sweeps and its shared-memory crossings on
@@ -37,19 +38,27 @@ __device__ __forceinline__ void cp8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
 }
 
-template <int N, int NSLOT>
+// NB = 1 adds the neighbour traffic and arithmetic of the real matvec: per cell 8 n^2 more values
+// (2 layers x 4 face neighbours in the two in-plane directions, taken as contiguous 2 n^2 chunks
+// of the tiles +-1 row and +-1 plane away, so they come from L2 like the real re-reads) copied
+// into the slot with the own tile; per plane 4 ghost lines get a mass sweep and are coupled
+// into b, and 4 x 2 neighbour values per row are coupled into a.
+template <int N, int NSLOT, int NB>
 __global__ void __launch_bounds__(128)
 k_plane_probe(const __grid_constant__ ProbeParams pp, const double* __restrict__ in,
-              double* __restrict__ out, int64_t ntiles) {
+              double* __restrict__ out, int64_t ntiles, int64_t trow, int64_t tplane) {
   constexpr int C = PPC<N>::C, NN = N * N, N3 = N * NN;
   constexpr int PK = NN | 1, CS = N * PK;
   constexpr int TE = C * N3, NCP = (TE + 31) / 32;
   constexpr int NP = C * N;                       // planes (one round)
   constexpr int L = C * NN, ZR = (L + 31) / 32;
-  constexpr int SLOT = C * CS + ((C * CS) & 1);
+  constexpr int SLOT0 = C * CS + ((C * CS) & 1);
+  constexpr int GH = NB ? 4 * C * 2 * NN : 0;      // ghost values per tile: 4 neighbours x 2 layers
+  constexpr int NGC = (GH + 31) / 32;
+  constexpr int SLOT = SLOT0 + GH + (GH & 1);
   extern __shared__ __align__(16) unsigned char pp_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* const slots = reinterpret_cast<double*>(pp_raw) + warp * ((NSLOT + 1) * SLOT);
+  double* const slots = reinterpret_cast<double*>(pp_raw) + warp * (NSLOT * SLOT + SLOT0);
   double* const Cb = slots + NSLOT * SLOT;        // the c field of the current tile
 
   int off[NCP];
@@ -72,6 +81,20 @@ k_plane_probe(const __grid_constant__ ProbeParams pp, const double* __restrict__
 #pragma unroll
     for (int m = 0; m < NCP; ++m)
       if (lane + 32 * m < TE) cp8(dst + off[m], src + lane + 32 * m);
+    if constexpr (NB) {
+      // ghost g = (f, cell, 2 n^2 values): neighbour tile f of {-row, +row, -plane, +plane}
+#pragma unroll
+      for (int m = 0; m < NGC; ++m) {
+        const int e = lane + 32 * m;
+        if (e < GH) {
+          const int f = e / (C * 2 * NN), r = e % (C * 2 * NN), c = r / (2 * NN), v = r % (2 * NN);
+          int64_t tn = t + (f == 0 ? -trow : (f == 1 ? trow : (f == 2 ? -tplane : tplane)));
+          if (tn < 0) tn += ntiles;
+          if (tn >= ntiles) tn -= ntiles;
+          cp8(dst + SLOT0 + e, in + tn * TE + c * N3 + ((f & 1) ? v : N3 - 2 * NN + v));
+        }
+      }
+    }
   };
 #pragma unroll
   for (int s = 0; s < NSLOT - 1; ++s) {
@@ -103,6 +126,25 @@ k_plane_probe(const __grid_constant__ ProbeParams pp, const double* __restrict__
         const auto sx = eo_split<N>(x);
         eo_mul<N, 1, false>(pp.A1, sx, tt[j]);
         eo_mul<N, 1, false>(pp.A2, sx, aa[j]);
+        if constexpr (NB) {   // 2 + 2 neighbour values of this row (the z+- layers)
+          const double* G = F + SLOT0 + (2 * C + lane / N) * 2 * NN + (lane % N) * N + j;
+          const double zm0 = G[0], zm1 = G[NN], zp0 = G[C * 2 * NN], zp1 = G[C * 2 * NN + NN];
+          aa[j][0] = fma(pp.A2[0], zm0, fma(pp.A2[1], zm1, aa[j][0]));
+          aa[j][1] = fma(pp.A2[2], zm0, fma(pp.A2[3], zm1, aa[j][1]));
+          aa[j][N - 2] = fma(pp.A2[4], zp0, fma(pp.A2[5], zp1, aa[j][N - 2]));
+          aa[j][N - 1] = fma(pp.A2[6], zp0, fma(pp.A2[7], zp1, aa[j][N - 1]));
+        }
+      }
+      double gy[4][N];        // M applied to the 4 ghost lines of this plane (the y+- layers)
+      if constexpr (NB) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          double x[N];
+          const double* G = F + SLOT0 + ((g >> 1) * C + lane / N) * 2 * NN + (g & 1) * NN + (lane % N) * N;
+#pragma unroll
+          for (int i = 0; i < N; ++i) x[i] = G[i];
+          eo_mul<N, 1, false>(pp.A1, eo_split<N>(x), gy[g]);
+        }
       }
 #pragma unroll
       for (int i = 0; i < N; ++i) {          // "y stage": b = A1 a + A2 t, c = A1 t per column
@@ -116,6 +158,12 @@ k_plane_probe(const __grid_constant__ ProbeParams pp, const double* __restrict__
         eo_mul<N, 1, false>(pp.A1, eo_split<N>(xa), b);
         eo_mul<N, 1, true>(pp.A2, st, b);
         eo_mul<N, 1, false>(pp.A1, st, c);
+        if constexpr (NB) {
+          b[0] = fma(pp.A2[0], gy[0][i], fma(pp.A2[1], gy[1][i], b[0]));
+          b[1] = fma(pp.A2[2], gy[0][i], fma(pp.A2[3], gy[1][i], b[1]));
+          b[N - 2] = fma(pp.A2[4], gy[2][i], fma(pp.A2[5], gy[3][i], b[N - 2]));
+          b[N - 1] = fma(pp.A2[6], gy[2][i], fma(pp.A2[7], gy[3][i], b[N - 1]));
+        }
 #pragma unroll
         for (int j = 0; j < N; ++j) {
           P[j * N + i] = b[j];
@@ -157,11 +205,12 @@ __global__ void k_probe_fill(double* a, int64_t n) {
   }
 }
 
-template <int N>
+template <int N, int NB>
 cudaError_t probe_n(double* gdofs, cudaStream_t s) {
-  constexpr int C = PPC<N>::C, N3 = N * N * N, NSLOT = 3;
-  constexpr int CS = N * ((N * N) | 1), SLOT = C * CS + ((C * CS) & 1);
-  constexpr int smem = 4 * (NSLOT + 1) * SLOT * 8;
+  constexpr int C = PPC<N>::C, N3 = N * N * N, NSLOT = (NB && N >= 6) ? 2 : 3;
+  constexpr int CS = N * ((N * N) | 1), SLOT0 = C * CS + ((C * CS) & 1);
+  constexpr int GH = NB ? 4 * C * 2 * N * N : 0, SLOT = SLOT0 + GH + (GH & 1);
+  constexpr int smem = 4 * (NSLOT * SLOT + SLOT0) * 8;
   const int64_t ntiles = (int64_t)(110.6e6 / (C * N3));       // ~110 M DoF like the C4 meshes
   const int64_t nd = ntiles * C * N3;
   double *a, *b;
@@ -178,7 +227,8 @@ cudaError_t probe_n(double* gdofs, cudaStream_t s) {
     pp.A1[k] = 0.25 + 0.01 * k;
     pp.A2[k] = -0.125 + 0.02 * k;
   }
-  auto kern = k_plane_probe<N, NSLOT>;
+  auto kern = k_plane_probe<N, NSLOT, NB>;
+  const int64_t trow = 480 / (N * C) + 1, tplane = trow * (480 / N);   // tiles per x-row / per plane of a C4-like mesh
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int dev = 0, sms = 0, bps = 0;
   cudaGetDevice(&dev);
@@ -193,7 +243,7 @@ cudaError_t probe_n(double* gdofs, cudaStream_t s) {
     for (int cap = 1; cap <= 2 && cap <= bps; ++cap) {        // one and two blocks per SM
       for (int rep = 0; rep < 4; ++rep) {
         cudaEventRecord(e0, s);
-        kern<<<sms * cap, 128, smem, s>>>(pp, a, b, ntiles);
+        kern<<<sms * cap, 128, smem, s>>>(pp, a, b, ntiles, trow, tplane);
         cudaEventRecord(e1, s);
         cudaEventSynchronize(e1);
         float ms;
@@ -213,15 +263,20 @@ cudaError_t probe_n(double* gdofs, cudaStream_t s) {
 
 }  // namespace
 
-// kind = 10 + n, n = 3..8: GDoF/s of the pipelined-plane matvec proxy (see the header)
+// kind = 10 + n, n = 3..8: GDoF/s of the pipelined-plane matvec proxy (see the header);
+// kind = 20 + n, n = 3..6: the same with the neighbour traffic and couplings (NB = 1)
 cudaError_t measure_plane_probe(int n, double* value, cudaStream_t s) {
   switch (n) {
-    case 3: return probe_n<3>(value, s);
-    case 4: return probe_n<4>(value, s);
-    case 5: return probe_n<5>(value, s);
-    case 6: return probe_n<6>(value, s);
-    case 7: return probe_n<7>(value, s);
-    case 8: return probe_n<8>(value, s);
+    case 3: return probe_n<3, 0>(value, s);
+    case 4: return probe_n<4, 0>(value, s);
+    case 5: return probe_n<5, 0>(value, s);
+    case 6: return probe_n<6, 0>(value, s);
+    case 7: return probe_n<7, 0>(value, s);
+    case 8: return probe_n<8, 0>(value, s);
+    case 13: return probe_n<3, 1>(value, s);
+    case 14: return probe_n<4, 1>(value, s);
+    case 15: return probe_n<5, 1>(value, s);
+    case 16: return probe_n<6, 1>(value, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -81,8 +81,9 @@ def test_plane_probe_runs():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_1907_08492_b200 as P
-    v = P.measure_peak("plane_probe_n4")
-    assert v > 1.0 and v < 1e4
+    for kind in ("plane_probe_n4", "plane_probe_nb_n4"):
+        v = P.measure_peak(kind)
+        assert v > 1.0 and v < 1e4
     import ctypes
     from paper_1907_08492_b200._lib import lib
     x = ctypes.c_double()
