@@ -54,7 +54,6 @@ k_plane_probe(const __grid_constant__ ProbeParams pp, const double* __restrict__
   constexpr int L = C * NN, ZR = (L + 31) / 32;
   constexpr int SLOT0 = C * CS + ((C * CS) & 1);
   constexpr int GH = NB ? 4 * C * 2 * NN : 0;      // ghost values per tile: 4 neighbours x 2 layers
-  constexpr int NGC = (GH + 31) / 32;
   constexpr int SLOT = SLOT0 + GH + (GH & 1);
   extern __shared__ __align__(16) unsigned char pp_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -82,16 +81,24 @@ k_plane_probe(const __grid_constant__ ProbeParams pp, const double* __restrict__
     for (int m = 0; m < NCP; ++m)
       if (lane + 32 * m < TE) cp8(dst + off[m], src + lane + 32 * m);
     if constexpr (NB) {
-      // ghost g = (f, cell, 2 n^2 values): neighbour tile f of {-row, +row, -plane, +plane}
+      // ghost g = (f, cell, 2 n^2 values): neighbour tile f of {-row, +row, -plane, +plane};
+      // even n copies pairs (16-byte cp.async), odd n single values
+      constexpr int GV = (N % 2 == 0) ? 2 : 1;
 #pragma unroll
-      for (int m = 0; m < NGC; ++m) {
-        const int e = lane + 32 * m;
+      for (int m = 0; m < (GH / GV + 31) / 32; ++m) {
+        const int e = (lane + 32 * m) * GV;
         if (e < GH) {
           const int f = e / (C * 2 * NN), r = e % (C * 2 * NN), c = r / (2 * NN), v = r % (2 * NN);
           int64_t tn = t + (f == 0 ? -trow : (f == 1 ? trow : (f == 2 ? -tplane : tplane)));
           if (tn < 0) tn += ntiles;
           if (tn >= ntiles) tn -= ntiles;
-          cp8(dst + SLOT0 + e, in + tn * TE + c * N3 + ((f & 1) ? v : N3 - 2 * NN + v));
+          const double* sp = in + tn * TE + c * N3 + ((f & 1) ? v : N3 - 2 * NN + v);
+          if constexpr (GV == 2) {
+            const unsigned da = (unsigned)__cvta_generic_to_shared(dst + SLOT0 + e);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(da), "l"(sp) : "memory");
+          } else {
+            cp8(dst + SLOT0 + e, sp);
+          }
         }
       }
     }
